@@ -1,0 +1,156 @@
+/*
+ * deft_b200.h -- C-ABI of the B200-native DeFT hot path (libdeft_b200.so).
+ *
+ * The reference (deftsim, pure Python) has no FFI; its drop-in boundary is the
+ * Python API.  Every entry point below replaces one piece of that API, cited as
+ * reference file:line (paths relative to /root/reference/pkg/src/deftsim):
+ *
+ *   subset-sum solver ...... naive_knapsack         knapsack.py:55-94
+ *                            recursive_knapsack     knapsack.py:97-127 (batched levels)
+ *   bucket communication ... the simulated link transfer  simulator.py:136-147, 184-196
+ *   delayed SGD update ..... the implicit update event    scheduler.py:56-61, 223-241;
+ *                                                         simulator.py:238-243
+ *
+ * Conventions: plain pointers and sizes, no torch types.  Every function
+ * returns 0 (DEFT_OK) or a negative deft_status_t; deft_last_error() gives the
+ * thread-local message.  The Python wrapper (paper_2503_16815_b200/_native.py)
+ * re-raises them as the matching DeftError subclass (errors.py:7-60).
+ * Pointers named d_* are device pointers; `stream` is a cudaStream_t passed as
+ * void* so this header needs no CUDA include.
+ */
+#ifndef DEFT_B200_H_
+#define DEFT_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t deft_status_t;
+#define DEFT_OK 0
+#define DEFT_ERR_INVALID_ARGUMENT (-1) /* -> DeftError            */
+#define DEFT_ERR_CUDA (-2)             /* -> DeviceError          */
+#define DEFT_ERR_WORKSPACE (-3)        /* -> DeviceError          */
+#define DEFT_ERR_UNSUPPORTED (-4)      /* -> DeviceError          */
+#define DEFT_ERR_PEER (-5)             /* -> DeviceError          */
+
+/* knapsack.py:16 */
+#define DEFT_MAX_EXACT_CAPACITY 10000000LL
+
+int32_t deft_abi_version(void);
+const char* deft_last_error(void);
+/* Number of kernels this library has launched in this process (all devices). */
+uint64_t deft_launch_count(void);
+
+/* ------------------------------------------------------------------------
+ * K1  batched subset-sum (weight == value) with include-earliest reconstruction.
+ *
+ * Problem p owns items [item_off[p], item_off[p+1]) of `weights`, ordered by
+ * ASCENDING bucket id, with ORIGINAL integer-us weights (> 0) and an original
+ * capacity cap[p] >= 1.  The kernel applies the reference's scaling
+ * (knapsack.py:47-52: q = ceil(cap/1e7), w' = ceil(w/q), cap' = cap // q, in
+ * IEEE double exactly as CPython evaluates it), builds the suffix bitsets
+ * (knapsack.py:72-78), takes the highest reachable sum (:79) and reconstructs
+ * the include-earliest optimum (:80-88).  take[i] = 1 for chosen items;
+ * best[p] = the optimum in SCALED units.
+ * ------------------------------------------------------------------------ */
+
+/* Workspace (bytes) for a batch, given host copies of item counts and caps. */
+size_t deft_subset_sum_workspace_bytes(int32_t batch, const int32_t* n_items,
+                                       const int64_t* caps);
+
+/* Stream-ordered solve on device buffers. d_item_off has batch+1 entries.
+ * d_ws must be at least deft_subset_sum_workspace_bytes() bytes; the host
+ * arrays n_items/caps are needed to lay the workspace out. */
+deft_status_t deft_subset_sum_batched(const int64_t* d_weights, const int32_t* d_item_off,
+                                      const int64_t* d_caps, int32_t batch,
+                                      const int32_t* n_items, const int64_t* caps,
+                                      uint8_t* d_take, int64_t* d_best, void* d_ws,
+                                      size_t ws_bytes, void* stream);
+
+/* Synchronous host convenience used by the Python scheduler: a solver owns a
+ * high-priority stream, pinned staging and a growing device workspace. */
+typedef struct deft_solver deft_solver;
+deft_status_t deft_solver_create(int32_t device, deft_solver** out);
+deft_status_t deft_solver_destroy(deft_solver* s);
+/* Host arrays in, host arrays out; one H2D copy, <= 2 launches, one D2H copy. */
+deft_status_t deft_solver_solve(deft_solver* s, int32_t batch, const int32_t* n_items,
+                                const int64_t* weights, const int64_t* caps,
+                                uint8_t* take_out, int64_t* best_out);
+/* Device time (ms) of the kernels of the last solve, measured with CUDA events. */
+float deft_solver_last_kernel_ms(const deft_solver* s);
+
+/* ------------------------------------------------------------------------
+ * Symmetric device memory for the NVLink/NVSwitch P2P channels.
+ * deft_mem_alloc returns a cudaMalloc'ed region plus its 64-byte CUDA IPC
+ * handle; peers map it with deft_mem_open (lazy peer access enabled).
+ * ------------------------------------------------------------------------ */
+#define DEFT_IPC_HANDLE_BYTES 64
+deft_status_t deft_mem_alloc(size_t bytes, void** d_ptr, uint8_t* ipc_handle_out);
+deft_status_t deft_mem_free(void* d_ptr);
+deft_status_t deft_mem_open(const uint8_t* ipc_handle, void** d_peer_ptr);
+deft_status_t deft_mem_close(void* d_peer_ptr);
+
+/* ------------------------------------------------------------------------
+ * Communicator: one per rank over W <= 8 ranks of one NVSwitch node.
+ *   grads[r]  : rank r's gradient arena (n_slots group buffers of `slot_elems`
+ *               elements each) -- what autograd writes, what peers read;
+ *   params[r] : rank r's flat parameter buffer (fp32, output-side bucket first);
+ *   flags[r]  : rank r's barrier flag area (deft_comm_flag_bytes()).
+ * Pointer arrays are HOST arrays of already-mapped device pointers (own
+ * pointer at index `rank`).
+ * ------------------------------------------------------------------------ */
+typedef struct deft_comm deft_comm;
+size_t deft_comm_flag_bytes(int32_t world);
+deft_status_t deft_comm_create(int32_t rank, int32_t world, void* const* grads,
+                               void* const* params, void* const* flags, int64_t slot_elems,
+                               int32_t n_slots, int32_t grad_dtype, deft_comm** out);
+deft_status_t deft_comm_destroy(deft_comm* c);
+
+/* grad_dtype codes */
+#define DEFT_DTYPE_F32 0
+#define DEFT_DTYPE_BF16 1
+
+/* Channel ids: the paper's fast / slow links become two NVLink channels. */
+#define DEFT_CHANNEL_SM 0 /* SM-driven P2P loads (ratio 1.0, "fast link")     */
+#define DEFT_CHANNEL_CE 1 /* copy engines + local SM reduce ("slow link", mu) */
+
+/* Reduce-scatter of bucket [offset, offset+numel) of group slot `slot`:
+ * rank r sums shard r over all ranks (fp32 accumulation) and writes it in
+ * place into its own slot.  Stream-ordered on `stream`; the cross-rank
+ * entry barrier is inside the kernel. Replaces the simulated transfer of one
+ * planned bucket (simulator.py:136-147). With world == 1 it is a no-op. */
+deft_status_t deft_bucket_reduce_scatter(deft_comm* c, int32_t channel, int32_t slot,
+                                         int64_t offset, int64_t numel, void* stream);
+
+/* Fused delayed SGD/momentum update of the owned shard + all-gather of the
+ * updated parameters to every rank (the update event, scheduler.py:56-61):
+ *   g = shard(slot) * grad_scale          (grad_scale = 1 / (W * merge_count))
+ *   v = momentum * v + g  ;  p -= lr * v  (torch.optim.SGD, dampening 0)
+ * and p is stored to every rank's params (P2P stores over NVLink).  `mom` is
+ * this rank's momentum buffer, indexed like params. Entry and exit barriers
+ * are inside the kernel. */
+deft_status_t deft_bucket_update(deft_comm* c, int32_t slot, int64_t offset, int64_t numel,
+                                 float lr, float momentum, float grad_scale, float* d_mom,
+                                 void* stream);
+
+/* Local (W == 1 or rank-private) fused update over device arrays:
+ * v = m*v + s*g ; p -= lr*v. grad_dtype as above. */
+deft_status_t deft_sgd_momentum_update(const void* d_grad, int32_t grad_dtype, float* d_param,
+                                       float* d_mom, int64_t numel, float lr, float momentum,
+                                       float grad_scale, void* stream);
+
+/* Multi-bucket variant: one launch updates `count` (offset, numel, scale)
+ * segments of the same arrays (the buckets of one update event). Host arrays. */
+deft_status_t deft_sgd_momentum_update_multi(const void* d_grad, int32_t grad_dtype,
+                                             float* d_param, float* d_mom, int32_t count,
+                                             const int64_t* offsets, const int64_t* numels,
+                                             const float* grad_scales, float lr,
+                                             float momentum, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DEFT_B200_H_ */

@@ -1,0 +1,436 @@
+// K2/K3/K4: gradient-bucket communication over NVLink / NVSwitch, fused with
+// the delayed SGD/momentum update, sm_100a.
+//
+// The reference only SIMULATES this step: a planned bucket occupies a link for
+// comm_fast_us * ratio (simulator.py:136-147, profiles.py:155-157) and a group
+// update is bookkeeping once its last bucket is sent (scheduler.py:56-61,
+// simulator.py:238-243).  Here it is real, split the way the delayed update
+// allows:
+//
+//  * at the DeFT-planned window (link stream)      -> reduce-scatter:
+//      rank r sums shard r of the bucket over all ranks, reading the peers'
+//      gradient slots directly over NVLink (SM channel, 128-bit loads, fp32
+//      accumulation) or pulling them with the copy engines first (CE channel),
+//      and writes the sum in place into its own slot;
+//  * at the update's visibility point (update stream) -> fused update + all-gather:
+//      v = m*v + g/(W*k); p -= lr*v on the owned shard, and the updated
+//      parameters are STORED into every rank's parameter buffer over NVLink.
+//    One pass over the shard, no separate elementwise kernel, momentum touched
+//    only for the owned 1/W shard.
+//
+// Cross-rank ordering: per-block barriers on system-scope flags.  Block b of
+// rank r only waits for block b of the peers (each block owns the same
+// sub-range on every rank), so no kernel ever waits for a whole peer grid.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace deft {
+
+constexpr int kCommThreads = 512;
+constexpr int kCommMaxBlocks = 32;      // leave the rest of the SMs to compute
+constexpr int kLocalThreads = 256;
+
+int comm_grid_for(int64_t elems_per_rank) {
+  const int64_t per_block = (int64_t)kCommThreads * 8 * 2;
+  int64_t g = (elems_per_rank + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > kCommMaxBlocks) g = kCommMaxBlocks;
+  return (int)g;
+}
+
+// ---- system-scope flag primitives -----------------------------------------
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Block-level barrier with the same-index block on every rank.
+__device__ __forceinline__ void peer_block_barrier(const PeerPtrs& P, int rank, int world,
+                                                   int set, int block, uint32_t value) {
+  __threadfence_system();
+  __syncthreads();
+  if ((int)threadIdx.x < world) {
+    const int peer = threadIdx.x;
+    const int64_t base = ((int64_t)set * kMaxCommBlocks + block) * kMaxWorld;
+    st_release_sys(P.flags[peer] + base + rank, value);
+    const uint32_t* mine = P.flags[rank] + base + peer;
+    // wrap-safe "mine >= value"
+    while ((int32_t)(ld_acquire_sys(mine) - value) < 0) {
+    }
+  }
+  __syncthreads();
+}
+
+// ---- element access helpers -----------------------------------------------
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+  static constexpr int N = 4;
+  using Raw = float4;
+  __device__ static void to_f32(const Raw& r, float* o) {
+    o[0] = r.x; o[1] = r.y; o[2] = r.z; o[3] = r.w;
+  }
+  __device__ static Raw from_f32(const float* o) { return make_float4(o[0], o[1], o[2], o[3]); }
+  __device__ static float scalar(const float* p) { return *p; }
+  __device__ static void put(float* p, float v) { *p = v; }
+};
+template <>
+struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  using Raw = uint4;
+  __device__ static void to_f32(const Raw& r, float* o) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __bfloat1622float2(h[k]);
+      o[2 * k] = f.x;
+      o[2 * k + 1] = f.y;
+    }
+  }
+  __device__ static Raw from_f32(const float* o) {
+    Raw r;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&r);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(o[2 * k], o[2 * k + 1]);
+    return r;
+  }
+  __device__ static float scalar(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+  __device__ static void put(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+};
+
+template <typename Raw>
+__device__ __forceinline__ Raw ld_nc(const Raw* p) {
+  return __ldg(p);
+}
+
+// Split [lo, hi) into an unaligned scalar head, an aligned vector body and a
+// scalar tail; block `blk` of `nblk` gets a contiguous share of the body.
+struct Span {
+  int64_t head_lo, head_hi, body_lo, body_hi, tail_lo, tail_hi;  // elements
+};
+template <int N>
+__device__ __forceinline__ Span split_span(int64_t lo, int64_t hi) {
+  Span s;
+  int64_t a = (lo + N - 1) / N * N;
+  if (a > hi) a = hi;
+  int64_t b = hi / N * N;
+  if (b < a) b = a;
+  s.head_lo = lo; s.head_hi = a; s.body_lo = a; s.body_hi = b; s.tail_lo = b; s.tail_hi = hi;
+  return s;
+}
+
+// ============================================================================
+// Reduce-scatter, SM channel: shard r = sum over ranks, written in place.
+// ============================================================================
+template <typename T>
+__global__ void __launch_bounds__(kCommThreads) reduce_scatter_kernel(
+    PeerPtrs P, int rank, int world, int64_t slot_base, int64_t lo, int64_t hi, uint32_t epoch) {
+  using V = Vec<T>;
+  peer_block_barrier(P, rank, world, kBarrierRS, blockIdx.x, epoch);
+  const T* src[kMaxWorld];
+#pragma unroll
+  for (int k = 0; k < kMaxWorld; ++k)
+    src[k] = k < world ? reinterpret_cast<const T*>(P.grads[k]) + slot_base : nullptr;
+  T* dst = reinterpret_cast<T*>(P.grads[rank]) + slot_base;
+
+  const Span s = split_span<V::N>(lo, hi);
+  // scalar head / tail: handled by block 0
+  if (blockIdx.x == 0) {
+    for (int64_t e = s.head_lo + threadIdx.x; e < s.head_hi; e += blockDim.x) {
+      float acc = 0.f;
+      for (int k = 0; k < world; ++k) acc += V::scalar(src[k] + e);
+      V::put(dst + e, acc);
+    }
+    for (int64_t e = s.tail_lo + threadIdx.x; e < s.tail_hi; e += blockDim.x) {
+      float acc = 0.f;
+      for (int k = 0; k < world; ++k) acc += V::scalar(src[k] + e);
+      V::put(dst + e, acc);
+    }
+  }
+  const int64_t nv = (s.body_hi - s.body_lo) / V::N;
+  const int64_t v0 = s.body_lo / V::N;
+  using Raw = typename V::Raw;
+  constexpr int U = 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride * U) {
+    Raw raw[U][kMaxWorld];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t vi = i + u * stride;
+#pragma unroll
+      for (int k = 0; k < kMaxWorld; ++k)
+        if (k < world && vi < nv) raw[u][k] = ld_nc(reinterpret_cast<const Raw*>(src[k]) + v0 + vi);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t vi = i + u * stride;
+      if (vi >= nv) break;
+      float acc[V::N], tmp[V::N];
+      V::to_f32(raw[u][0], acc);
+#pragma unroll
+      for (int k = 1; k < kMaxWorld; ++k) {
+        if (k < world) {
+          V::to_f32(raw[u][k], tmp);
+#pragma unroll
+          for (int c = 0; c < V::N; ++c) acc[c] += tmp[c];
+        }
+      }
+      reinterpret_cast<Raw*>(dst)[v0 + vi] = V::from_f32(acc);
+    }
+  }
+}
+
+cudaError_t launch_reduce_scatter_sm(const PeerPtrs& P, int rank, int world, int dtype,
+                                     int64_t slot_base, int64_t offset, int64_t numel,
+                                     uint32_t epoch, cudaStream_t stream) {
+  const int align = dtype == 0 ? 4 : 8;
+  const ShardRange sh = shard_of(offset, numel, rank, world, align);
+  const int grid = comm_grid_for((numel + world - 1) / world);
+  if (dtype == 0)
+    reduce_scatter_kernel<float><<<grid, kCommThreads, 0, stream>>>(P, rank, world, slot_base,
+                                                                   sh.lo, sh.hi, epoch);
+  else
+    reduce_scatter_kernel<__nv_bfloat16><<<grid, kCommThreads, 0, stream>>>(
+        P, rank, world, slot_base, sh.lo, sh.hi, epoch);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// Barrier-only kernel (CE channel: the copy engines cannot wait on a flag).
+// ============================================================================
+__global__ void barrier_kernel(PeerPtrs P, int rank, int world, int set, uint32_t epoch) {
+  peer_block_barrier(P, rank, world, set, 0, epoch);
+}
+
+cudaError_t launch_barrier(const PeerPtrs& P, int rank, int world, int set, uint32_t epoch,
+                           cudaStream_t stream) {
+  barrier_kernel<<<1, 32, 0, stream>>>(P, rank, world, set, epoch);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// CE channel local reduce: own shard += staged peer shards.
+template <typename T>
+__global__ void __launch_bounds__(kLocalThreads) ce_reduce_kernel(
+    T* own, const T* staging, int world, int rank, int64_t len, int64_t stride_elems) {
+  using V = Vec<T>;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float acc = V::scalar(own + e);
+    int slot = 0;
+    for (int k = 0; k < world; ++k) {
+      if (k == rank) continue;
+      acc += V::scalar(staging + (int64_t)slot * stride_elems + e);
+      ++slot;
+    }
+    V::put(own + e, acc);
+  }
+}
+
+cudaError_t launch_ce_reduce(char* own_grad_slot, const char* staging, int dtype, int world,
+                             int rank, int64_t shard_lo, int64_t shard_len,
+                             int64_t staging_stride_elems, cudaStream_t stream) {
+  if (shard_len <= 0) return cudaSuccess;
+  int grid = (int)((shard_len + kLocalThreads * 4 - 1) / (kLocalThreads * 4));
+  if (grid > 148 * 4) grid = 148 * 4;
+  if (dtype == 0)
+    ce_reduce_kernel<float><<<grid, kLocalThreads, 0, stream>>>(
+        reinterpret_cast<float*>(own_grad_slot) + shard_lo,
+        reinterpret_cast<const float*>(staging), world, rank, shard_len, staging_stride_elems);
+  else
+    ce_reduce_kernel<__nv_bfloat16><<<grid, kLocalThreads, 0, stream>>>(
+        reinterpret_cast<__nv_bfloat16*>(own_grad_slot) + shard_lo,
+        reinterpret_cast<const __nv_bfloat16*>(staging), world, rank, shard_len,
+        staging_stride_elems);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// Fused delayed SGD/momentum update of the owned shard + parameter all-gather.
+// ============================================================================
+template <typename T>
+__global__ void __launch_bounds__(kCommThreads) update_allgather_kernel(
+    PeerPtrs P, int rank, int world, int64_t slot_base, int64_t lo, int64_t hi, float lr,
+    float momentum, float scale, float* __restrict__ mom, uint32_t epoch) {
+  using V = Vec<T>;
+  // entry: every rank's no-read window for this bucket is open
+  if (world > 1) peer_block_barrier(P, rank, world, kBarrierUpdate, blockIdx.x, 2u * epoch + 1u);
+  const T* g = reinterpret_cast<const T*>(P.grads[rank]) + slot_base;
+  float* own = P.params[rank];
+
+  auto step = [&](int64_t e, float gv) {
+    const float v = fmaf(momentum, mom[e], gv * scale);
+    mom[e] = v;
+    const float p = fmaf(-lr, v, own[e]);
+    for (int k = 0; k < world; ++k) P.params[k][e] = p;
+  };
+  // scalar edges (parameters are fp32: 4-element alignment)
+  const Span s = split_span<4>(lo, hi);
+  if (blockIdx.x == 0) {
+    for (int64_t e = s.head_lo + threadIdx.x; e < s.head_hi; e += blockDim.x) step(e, V::scalar(g + e));
+    for (int64_t e = s.tail_lo + threadIdx.x; e < s.tail_hi; e += blockDim.x) step(e, V::scalar(g + e));
+  }
+  const int64_t nv = (s.body_hi - s.body_lo) / 4;
+  const int64_t v0 = s.body_lo / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    const int64_t e = (v0 + i) * 4;
+    float gv[4];
+    if constexpr (sizeof(T) == 4) {
+      const float4 r = *reinterpret_cast<const float4*>(g + e);
+      gv[0] = r.x; gv[1] = r.y; gv[2] = r.z; gv[3] = r.w;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) gv[c] = V::scalar(g + e + c);
+    }
+    const float4 m4 = *reinterpret_cast<const float4*>(mom + e);
+    const float4 p4 = *reinterpret_cast<const float4*>(own + e);
+    float4 v4, q4;
+    v4.x = fmaf(momentum, m4.x, gv[0] * scale);
+    v4.y = fmaf(momentum, m4.y, gv[1] * scale);
+    v4.z = fmaf(momentum, m4.z, gv[2] * scale);
+    v4.w = fmaf(momentum, m4.w, gv[3] * scale);
+    q4.x = fmaf(-lr, v4.x, p4.x);
+    q4.y = fmaf(-lr, v4.y, p4.y);
+    q4.z = fmaf(-lr, v4.z, p4.z);
+    q4.w = fmaf(-lr, v4.w, p4.w);
+    *reinterpret_cast<float4*>(mom + e) = v4;
+#pragma unroll
+    for (int k = 0; k < kMaxWorld; ++k)
+      if (k < world) *reinterpret_cast<float4*>(P.params[k] + e) = q4;
+  }
+  // exit: every rank's stores into every parameter buffer have landed
+  if (world > 1) peer_block_barrier(P, rank, world, kBarrierUpdate, blockIdx.x, 2u * epoch + 2u);
+}
+
+cudaError_t launch_update_allgather(const PeerPtrs& P, int rank, int world, int dtype,
+                                    int64_t slot_base, int64_t offset, int64_t numel, float lr,
+                                    float momentum, float grad_scale, float* mom,
+                                    uint32_t epoch, cudaStream_t stream) {
+  const ShardRange sh = shard_of(offset, numel, rank, world, dtype == 0 ? 4 : 8);
+  const int grid = comm_grid_for((numel + world - 1) / world);
+  if (dtype == 0)
+    update_allgather_kernel<float><<<grid, kCommThreads, 0, stream>>>(
+        P, rank, world, slot_base, sh.lo, sh.hi, lr, momentum, grad_scale, mom, epoch);
+  else
+    update_allgather_kernel<__nv_bfloat16><<<grid, kCommThreads, 0, stream>>>(
+        P, rank, world, slot_base, sh.lo, sh.hi, lr, momentum, grad_scale, mom, epoch);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// Local fused update (W == 1): one launch covers up to kMaxSeg buckets.
+// ============================================================================
+constexpr int kMaxSeg = 32;
+struct SegTable {
+  int64_t off[kMaxSeg];
+  int64_t len[kMaxSeg];
+  int64_t first_vec[kMaxSeg + 1];  // prefix of per-segment work units
+  float scale[kMaxSeg];
+  int32_t count;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kLocalThreads) sgd_local_kernel(
+    const T* __restrict__ grad, float* __restrict__ param, float* __restrict__ mom, SegTable t,
+    float lr, float momentum) {
+  using V = Vec<T>;
+  const int64_t total = t.first_vec[t.count];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int seg = 0;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < total; u += stride) {
+    while (u >= t.first_vec[seg + 1]) ++seg;
+    // unit u covers 4 consecutive elements of segment `seg`, from its aligned start
+    const int64_t base = t.off[seg];
+    const int64_t end = base + t.len[seg];
+    const int64_t aligned = (base + 3) / 4 * 4;
+    const int64_t k = u - t.first_vec[seg];
+    const float s = t.scale[seg];
+    if (k == 0 && aligned > base) {  // unit 0 also owns the unaligned head
+      for (int64_t e = base; e < aligned && e < end; ++e) {
+        const float v = fmaf(momentum, mom[e], V::scalar(grad + e) * s);
+        mom[e] = v;
+        param[e] = fmaf(-lr, v, param[e]);
+      }
+    }
+    const int64_t e = aligned + k * 4;
+    if (e + 4 <= end) {
+      float gv[4];
+      if constexpr (sizeof(T) == 4) {
+        const float4 r = __ldg(reinterpret_cast<const float4*>(grad + e));
+        gv[0] = r.x; gv[1] = r.y; gv[2] = r.z; gv[3] = r.w;
+      } else {
+        const uint2 r = __ldg(reinterpret_cast<const uint2*>(grad + e));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+        const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+        gv[0] = a.x; gv[1] = a.y; gv[2] = b.x; gv[3] = b.y;
+      }
+      float4 m4 = *reinterpret_cast<const float4*>(mom + e);
+      float4 p4 = *reinterpret_cast<const float4*>(param + e);
+      m4.x = fmaf(momentum, m4.x, gv[0] * s);
+      m4.y = fmaf(momentum, m4.y, gv[1] * s);
+      m4.z = fmaf(momentum, m4.z, gv[2] * s);
+      m4.w = fmaf(momentum, m4.w, gv[3] * s);
+      p4.x = fmaf(-lr, m4.x, p4.x);
+      p4.y = fmaf(-lr, m4.y, p4.y);
+      p4.z = fmaf(-lr, m4.z, p4.z);
+      p4.w = fmaf(-lr, m4.w, p4.w);
+      *reinterpret_cast<float4*>(mom + e) = m4;
+      *reinterpret_cast<float4*>(param + e) = p4;
+    } else {
+      for (int64_t x = e; x < end; ++x) {  // tail
+        const float v = fmaf(momentum, mom[x], V::scalar(grad + x) * s);
+        mom[x] = v;
+        param[x] = fmaf(-lr, v, param[x]);
+      }
+    }
+  }
+}
+
+cudaError_t launch_sgd_local(const void* grad, int dtype, float* param, float* mom,
+                             int32_t count, const int64_t* offsets, const int64_t* numels,
+                             const float* scales, float lr, float momentum,
+                             cudaStream_t stream) {
+  for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
+    SegTable t{};
+    t.count = count - s0 < kMaxSeg ? count - s0 : kMaxSeg;
+    t.first_vec[0] = 0;
+    for (int k = 0; k < t.count; ++k) {
+      t.off[k] = offsets[s0 + k];
+      t.len[k] = numels[s0 + k];
+      t.scale[k] = scales[s0 + k];
+      const int64_t aligned = (t.off[k] + 3) / 4 * 4;
+      const int64_t end = t.off[k] + t.len[k];
+      int64_t units = end > aligned ? (end - aligned + 3) / 4 : 0;
+      if (units == 0 && t.len[k] > 0) units = 1;  // head-only segment
+      t.first_vec[k + 1] = t.first_vec[k] + units;
+    }
+    const int64_t total = t.first_vec[t.count];
+    if (total == 0) continue;
+    int64_t grid = (total + kLocalThreads - 1) / kLocalThreads;
+    if (grid > 148 * 8) grid = 148 * 8;
+    if (dtype == 0)
+      sgd_local_kernel<float><<<(int)grid, kLocalThreads, 0, stream>>>(
+          reinterpret_cast<const float*>(grad), param, mom, t, lr, momentum);
+    else
+      sgd_local_kernel<__nv_bfloat16><<<(int)grid, kLocalThreads, 0, stream>>>(
+          reinterpret_cast<const __nv_bfloat16*>(grad), param, mom, t, lr, momentum);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace deft

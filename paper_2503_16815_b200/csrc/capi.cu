@@ -1,0 +1,468 @@
+// C-ABI of libdeft_b200.so (declared in include/deft_b200.h).
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "../../include/deft_b200.h"
+#include "common.cuh"
+
+namespace deft {
+static std::atomic<uint64_t> g_launches{0};
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace deft
+
+using namespace deft;
+
+static thread_local std::string g_err;
+
+static deft_status_t fail(deft_status_t code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+static deft_status_t cuda_fail(cudaError_t e, const char* where) {
+  return fail(DEFT_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define DEFT_CUDA(call)                                  \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+  } while (0)
+
+extern "C" int32_t deft_abi_version(void) { return 1; }
+extern "C" const char* deft_last_error(void) { return g_err.c_str(); }
+extern "C" uint64_t deft_launch_count(void) { return g_launches.load(); }
+
+// ============================================================================
+// K1 subset-sum
+// ============================================================================
+namespace {
+struct Layout {
+  std::vector<int64_t> row_off, meta_off;
+  std::vector<int32_t> small, large;
+  int64_t max_small_words = 0;
+  size_t rows_words = 0, meta_ints = 0;
+};
+
+deft_status_t plan_layout(int32_t batch, const int32_t* n_items, const int64_t* caps, Layout* L) {
+  L->row_off.assign(batch + 1, 0);
+  L->meta_off.assign(batch + 1, 0);
+  for (int32_t p = 0; p < batch; ++p) {
+    if (n_items[p] < 1) return fail(DEFT_ERR_INVALID_ARGUMENT, "subset-sum: empty problem");
+    if (caps[p] < 1) return fail(DEFT_ERR_INVALID_ARGUMENT, "subset-sum: capacity must be >= 1");
+    const int64_t words = host_row_words(caps[p]);
+    L->row_off[p + 1] = L->row_off[p] + (int64_t)(n_items[p] + 1) * words;
+    L->meta_off[p + 1] = L->meta_off[p] + 2 * (int64_t)(n_items[p] + 1);
+    if (words <= smem_words_limit()) {
+      L->small.push_back(p);
+      L->max_small_words = std::max(L->max_small_words, words);
+    } else {
+      L->large.push_back(p);
+    }
+  }
+  L->rows_words = (size_t)L->row_off[batch];
+  L->meta_ints = (size_t)L->meta_off[batch];
+  return DEFT_OK;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// workspace: rows | meta | row_off | meta_off | pids
+size_t ws_bytes_for(const Layout& L, int32_t batch) {
+  size_t b = align_up(L.rows_words * 4, 256);
+  b += align_up(L.meta_ints * 4, 256);
+  b += 2 * align_up((size_t)(batch + 1) * 8, 256);
+  b += align_up((size_t)batch * 4, 256);
+  return b;
+}
+}  // namespace
+
+extern "C" size_t deft_subset_sum_workspace_bytes(int32_t batch, const int32_t* n_items,
+                                                  const int64_t* caps) {
+  Layout L;
+  if (batch <= 0 || plan_layout(batch, n_items, caps, &L) != DEFT_OK) return 0;
+  return ws_bytes_for(L, batch);
+}
+
+static deft_status_t launch_with_layout(const Layout& L, const int64_t* d_weights,
+                                        const int32_t* d_item_off, const int64_t* d_caps,
+                                        int32_t batch, uint8_t* d_take, int64_t* d_best,
+                                        char* ws, cudaStream_t stream, bool upload_tables) {
+  char* cur = ws;
+  uint32_t* rows = reinterpret_cast<uint32_t*>(cur);
+  cur += align_up(L.rows_words * 4, 256);
+  int32_t* meta = reinterpret_cast<int32_t*>(cur);
+  cur += align_up(L.meta_ints * 4, 256);
+  int64_t* d_row_off = reinterpret_cast<int64_t*>(cur);
+  cur += align_up((size_t)(batch + 1) * 8, 256);
+  int64_t* d_meta_off = reinterpret_cast<int64_t*>(cur);
+  cur += align_up((size_t)(batch + 1) * 8, 256);
+  int32_t* d_pids = reinterpret_cast<int32_t*>(cur);
+  if (upload_tables) {
+    DEFT_CUDA(cudaMemcpyAsync(d_row_off, L.row_off.data(), (batch + 1) * 8,
+                              cudaMemcpyHostToDevice, stream));
+    DEFT_CUDA(cudaMemcpyAsync(d_meta_off, L.meta_off.data(), (batch + 1) * 8,
+                              cudaMemcpyHostToDevice, stream));
+    std::vector<int32_t> pids(L.small);
+    pids.insert(pids.end(), L.large.begin(), L.large.end());
+    DEFT_CUDA(cudaMemcpyAsync(d_pids, pids.data(), pids.size() * 4, cudaMemcpyHostToDevice,
+                              stream));
+    // the host vectors must outlive the copies
+    DEFT_CUDA(cudaStreamSynchronize(stream));
+  }
+  SubsetSumLaunch S{};
+  S.weights = d_weights;
+  S.item_off = d_item_off;
+  S.caps = d_caps;
+  S.row_off = d_row_off;
+  S.meta_off = d_meta_off;
+  S.rows = rows;
+  S.meta = meta;
+  S.take = d_take;
+  S.best = d_best;
+  S.pids_small = d_pids;
+  S.n_small = (int32_t)L.small.size();
+  S.max_small_words = L.max_small_words;
+  S.pids_large = d_pids + L.small.size();
+  S.n_large = (int32_t)L.large.size();
+  cudaError_t e = launch_subset_sum(S, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "subset_sum_kernel");
+  return DEFT_OK;
+}
+
+extern "C" deft_status_t deft_subset_sum_batched(const int64_t* d_weights,
+                                                 const int32_t* d_item_off,
+                                                 const int64_t* d_caps, int32_t batch,
+                                                 const int32_t* n_items, const int64_t* caps,
+                                                 uint8_t* d_take, int64_t* d_best, void* d_ws,
+                                                 size_t ws_bytes, void* stream) {
+  if (batch <= 0) return DEFT_OK;
+  Layout L;
+  deft_status_t st = plan_layout(batch, n_items, caps, &L);
+  if (st != DEFT_OK) return st;
+  if (ws_bytes < ws_bytes_for(L, batch))
+    return fail(DEFT_ERR_WORKSPACE, "subset-sum: workspace too small");
+  return launch_with_layout(L, d_weights, d_item_off, d_caps, batch, d_take, d_best,
+                            reinterpret_cast<char*>(d_ws), (cudaStream_t)stream, true);
+}
+
+struct deft_solver {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  char* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  char* dev = nullptr;  // inputs + outputs + workspace
+  size_t dev_bytes = 0;
+  float last_ms = 0.f;
+};
+
+static deft_status_t grow(deft_solver* s, size_t pinned_need, size_t dev_need) {
+  if (pinned_need > s->pinned_bytes) {
+    if (s->pinned) cudaFreeHost(s->pinned);
+    size_t nb = std::max(pinned_need, s->pinned_bytes * 2);
+    DEFT_CUDA(cudaMallocHost(&s->pinned, nb));
+    s->pinned_bytes = nb;
+  }
+  if (dev_need > s->dev_bytes) {
+    if (s->dev) cudaFree(s->dev);
+    size_t nb = std::max(dev_need, s->dev_bytes * 2);
+    DEFT_CUDA(cudaMalloc(&s->dev, nb));
+    s->dev_bytes = nb;
+  }
+  return DEFT_OK;
+}
+
+extern "C" deft_status_t deft_solver_create(int32_t device, deft_solver** out) {
+  if (!out) return fail(DEFT_ERR_INVALID_ARGUMENT, "null out");
+  deft_solver* s = new deft_solver();
+  s->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete s;
+    return cuda_fail(e, "cudaSetDevice");
+  }
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  e = cudaStreamCreateWithPriority(&s->stream, cudaStreamNonBlocking, hi);
+  if (e == cudaSuccess) e = cudaEventCreate(&s->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&s->ev1);
+  if (e != cudaSuccess) {
+    delete s;
+    return cuda_fail(e, "deft_solver_create");
+  }
+  *out = s;
+  return DEFT_OK;
+}
+
+extern "C" deft_status_t deft_solver_destroy(deft_solver* s) {
+  if (!s) return DEFT_OK;
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  if (s->pinned) cudaFreeHost(s->pinned);
+  if (s->dev) cudaFree(s->dev);
+  if (s->ev0) cudaEventDestroy(s->ev0);
+  if (s->ev1) cudaEventDestroy(s->ev1);
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+  return DEFT_OK;
+}
+
+extern "C" float deft_solver_last_kernel_ms(const deft_solver* s) { return s ? s->last_ms : 0.f; }
+
+extern "C" deft_status_t deft_solver_solve(deft_solver* s, int32_t batch, const int32_t* n_items,
+                                           const int64_t* weights, const int64_t* caps,
+                                           uint8_t* take_out, int64_t* best_out) {
+  if (!s) return fail(DEFT_ERR_INVALID_ARGUMENT, "null solver");
+  if (batch <= 0) return DEFT_OK;
+  Layout L;
+  deft_status_t st = plan_layout(batch, n_items, caps, &L);
+  if (st != DEFT_OK) return st;
+  int64_t total_items = 0;
+  for (int32_t p = 0; p < batch; ++p) total_items += n_items[p];
+  // pinned staging: weights | item_off | caps | row_off | meta_off | pids  ||  take | best
+  const size_t b_w = align_up(total_items * 8, 256), b_io = align_up((batch + 1) * 4, 256);
+  const size_t b_caps = align_up(batch * 8, 256), b_tab = align_up((batch + 1) * 8, 256);
+  const size_t b_pids = align_up(batch * 4, 256);
+  const size_t in_bytes = b_w + b_io + b_caps + 2 * b_tab + b_pids;
+  const size_t b_take = align_up(total_items, 256), b_best = align_up(batch * 8, 256);
+  const size_t out_bytes = b_take + b_best;
+  const size_t ws = align_up(L.rows_words * 4, 256) + align_up(L.meta_ints * 4, 256);
+  if (cudaSetDevice(s->device) != cudaSuccess) return fail(DEFT_ERR_CUDA, "cudaSetDevice");
+  st = grow(s, in_bytes + out_bytes, in_bytes + out_bytes + ws);
+  if (st != DEFT_OK) return st;
+
+  char* h = s->pinned;
+  memcpy(h, weights, total_items * 8);
+  int32_t* io = reinterpret_cast<int32_t*>(h + b_w);
+  io[0] = 0;
+  for (int32_t p = 0; p < batch; ++p) io[p + 1] = io[p] + n_items[p];
+  memcpy(h + b_w + b_io, caps, batch * 8);
+  memcpy(h + b_w + b_io + b_caps, L.row_off.data(), (batch + 1) * 8);
+  memcpy(h + b_w + b_io + b_caps + b_tab, L.meta_off.data(), (batch + 1) * 8);
+  int32_t* pids = reinterpret_cast<int32_t*>(h + b_w + b_io + b_caps + 2 * b_tab);
+  size_t k = 0;
+  for (int32_t p : L.small) pids[k++] = p;
+  for (int32_t p : L.large) pids[k++] = p;
+
+  char* d = s->dev;
+  DEFT_CUDA(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, s->stream));
+  SubsetSumLaunch S{};
+  S.weights = reinterpret_cast<const int64_t*>(d);
+  S.item_off = reinterpret_cast<const int32_t*>(d + b_w);
+  S.caps = reinterpret_cast<const int64_t*>(d + b_w + b_io);
+  S.row_off = reinterpret_cast<const int64_t*>(d + b_w + b_io + b_caps);
+  S.meta_off = reinterpret_cast<const int64_t*>(d + b_w + b_io + b_caps + b_tab);
+  const int32_t* d_pids = reinterpret_cast<const int32_t*>(d + b_w + b_io + b_caps + 2 * b_tab);
+  S.pids_small = d_pids;
+  S.n_small = (int32_t)L.small.size();
+  S.max_small_words = L.max_small_words;
+  S.pids_large = d_pids + L.small.size();
+  S.n_large = (int32_t)L.large.size();
+  char* d_out = d + in_bytes;
+  S.take = reinterpret_cast<uint8_t*>(d_out);
+  S.best = reinterpret_cast<int64_t*>(d_out + b_take);
+  char* wsp = d_out + out_bytes;
+  S.rows = reinterpret_cast<uint32_t*>(wsp);
+  S.meta = reinterpret_cast<int32_t*>(wsp + align_up(L.rows_words * 4, 256));
+  DEFT_CUDA(cudaEventRecord(s->ev0, s->stream));
+  cudaError_t e = launch_subset_sum(S, s->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "subset_sum_kernel");
+  DEFT_CUDA(cudaEventRecord(s->ev1, s->stream));
+  char* h_out = h + in_bytes;
+  DEFT_CUDA(cudaMemcpyAsync(h_out, d_out, out_bytes, cudaMemcpyDeviceToHost, s->stream));
+  DEFT_CUDA(cudaStreamSynchronize(s->stream));
+  cudaEventElapsedTime(&s->last_ms, s->ev0, s->ev1);
+  memcpy(take_out, h_out, total_items);
+  memcpy(best_out, h_out + b_take, batch * 8);
+  return DEFT_OK;
+}
+
+// ============================================================================
+// Symmetric memory (CUDA IPC)
+// ============================================================================
+extern "C" deft_status_t deft_mem_alloc(size_t bytes, void** d_ptr, uint8_t* ipc_handle_out) {
+  if (!d_ptr || bytes == 0) return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_mem_alloc");
+  DEFT_CUDA(cudaMalloc(d_ptr, bytes));
+  DEFT_CUDA(cudaMemset(*d_ptr, 0, bytes));
+  if (ipc_handle_out) {
+    cudaIpcMemHandle_t h;
+    DEFT_CUDA(cudaIpcGetMemHandle(&h, *d_ptr));
+    memcpy(ipc_handle_out, &h, sizeof(h));
+  }
+  return DEFT_OK;
+}
+extern "C" deft_status_t deft_mem_free(void* d_ptr) {
+  DEFT_CUDA(cudaFree(d_ptr));
+  return DEFT_OK;
+}
+extern "C" deft_status_t deft_mem_open(const uint8_t* ipc_handle, void** d_peer_ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  DEFT_CUDA(cudaIpcOpenMemHandle(d_peer_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return DEFT_OK;
+}
+extern "C" deft_status_t deft_mem_close(void* d_peer_ptr) {
+  DEFT_CUDA(cudaIpcCloseMemHandle(d_peer_ptr));
+  return DEFT_OK;
+}
+
+// ============================================================================
+// Communicator
+// ============================================================================
+struct deft_comm {
+  int rank = 0, world = 1, dtype = 0, n_slots = 0;
+  int64_t slot_elems = 0;
+  PeerPtrs P{};
+  uint32_t epoch_rs = 0, epoch_ce = 0, epoch_up = 0;
+  char* staging = nullptr;  // CE channel: (W-1) peer shards
+  size_t staging_bytes = 0;
+};
+
+extern "C" size_t deft_comm_flag_bytes(int32_t world) {
+  (void)world;
+  return (size_t)kNumBarrierSets * kMaxCommBlocks * kMaxWorld * sizeof(uint32_t);
+}
+
+extern "C" deft_status_t deft_comm_create(int32_t rank, int32_t world, void* const* grads,
+                                          void* const* params, void* const* flags,
+                                          int64_t slot_elems, int32_t n_slots,
+                                          int32_t grad_dtype, deft_comm** out) {
+  if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world || !out)
+    return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_comm_create: bad rank/world");
+  if (grad_dtype != DEFT_DTYPE_F32 && grad_dtype != DEFT_DTYPE_BF16)
+    return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_comm_create: bad dtype");
+  deft_comm* c = new deft_comm();
+  c->rank = rank;
+  c->world = world;
+  c->dtype = grad_dtype;
+  c->slot_elems = slot_elems;
+  c->n_slots = n_slots;
+  for (int r = 0; r < world; ++r) {
+    c->P.grads[r] = reinterpret_cast<char*>(grads[r]);
+    c->P.params[r] = reinterpret_cast<float*>(params[r]);
+    c->P.flags[r] = flags ? reinterpret_cast<uint32_t*>(flags[r]) : nullptr;
+    if (world > 1 && !c->P.flags[r]) {
+      delete c;
+      return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_comm_create: flags required for world > 1");
+    }
+  }
+  *out = c;
+  return DEFT_OK;
+}
+
+extern "C" deft_status_t deft_comm_destroy(deft_comm* c) {
+  if (!c) return DEFT_OK;
+  if (c->staging) cudaFree(c->staging);
+  delete c;
+  return DEFT_OK;
+}
+
+static deft_status_t check_range(const deft_comm* c, int32_t slot, int64_t offset, int64_t numel) {
+  if (slot < 0 || slot >= c->n_slots) return fail(DEFT_ERR_INVALID_ARGUMENT, "bad slot");
+  if (offset < 0 || numel < 0 || offset + numel > c->slot_elems)
+    return fail(DEFT_ERR_INVALID_ARGUMENT, "bucket range outside the gradient slot");
+  return DEFT_OK;
+}
+
+extern "C" deft_status_t deft_bucket_reduce_scatter(deft_comm* c, int32_t channel, int32_t slot,
+                                                    int64_t offset, int64_t numel,
+                                                    void* stream) {
+  if (!c) return fail(DEFT_ERR_INVALID_ARGUMENT, "null comm");
+  deft_status_t st = check_range(c, slot, offset, numel);
+  if (st != DEFT_OK) return st;
+  if (c->world == 1 || numel == 0) return DEFT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t slot_base = (int64_t)slot * c->slot_elems;
+  if (channel == DEFT_CHANNEL_SM) {
+    cudaError_t e = launch_reduce_scatter_sm(c->P, c->rank, c->world, c->dtype, slot_base, offset,
+                                             numel, ++c->epoch_rs, s);
+    if (e != cudaSuccess) return cuda_fail(e, "reduce_scatter_kernel");
+    return DEFT_OK;
+  }
+  if (channel != DEFT_CHANNEL_CE) return fail(DEFT_ERR_INVALID_ARGUMENT, "bad channel");
+  // copy-engine channel: barrier, (W-1) peer->local DMA copies, local SM reduce
+  const int esz = c->dtype == DEFT_DTYPE_F32 ? 4 : 2;
+  const ShardRange sh = shard_of(offset, numel, c->rank, c->world, c->dtype == 0 ? 4 : 8);
+  const int64_t len = sh.hi - sh.lo;
+  const int64_t per = (numel + c->world - 1) / c->world + 16;
+  const size_t need = (size_t)(c->world - 1) * per * esz;
+  if (need > c->staging_bytes) {
+    if (c->staging) {
+      DEFT_CUDA(cudaStreamSynchronize(s));
+      cudaFree(c->staging);
+    }
+    DEFT_CUDA(cudaMalloc(&c->staging, need));
+    c->staging_bytes = need;
+  }
+  cudaError_t e = launch_barrier(c->P, c->rank, c->world, kBarrierCE, ++c->epoch_ce, s);
+  if (e != cudaSuccess) return cuda_fail(e, "barrier_kernel");
+  if (len > 0) {
+    int k = 0;
+    for (int r = 0; r < c->world; ++r) {
+      if (r == c->rank) continue;
+      const char* src = c->P.grads[r] + (slot_base + sh.lo) * esz;
+      DEFT_CUDA(cudaMemcpyAsync(c->staging + (size_t)k * per * esz, src, (size_t)len * esz,
+                                cudaMemcpyDeviceToDevice, s));
+      ++k;
+    }
+  }
+  e = launch_ce_reduce(c->P.grads[c->rank] + slot_base * esz, c->staging, c->dtype, c->world,
+                       c->rank, sh.lo, len, per, s);
+  if (e != cudaSuccess) return cuda_fail(e, "ce_reduce_kernel");
+  // peers must be done pulling from us before our slot can change again: the
+  // update kernel's entry barrier orders that (see bucket_comm.cu).
+  return DEFT_OK;
+}
+
+extern "C" deft_status_t deft_bucket_update(deft_comm* c, int32_t slot, int64_t offset,
+                                           int64_t numel, float lr, float momentum,
+                                           float grad_scale, float* d_mom, void* stream) {
+  if (!c) return fail(DEFT_ERR_INVALID_ARGUMENT, "null comm");
+  deft_status_t st = check_range(c, slot, offset, numel);
+  if (st != DEFT_OK) return st;
+  if (numel == 0) return DEFT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t slot_base = (int64_t)slot * c->slot_elems;
+  if (c->world == 1) {
+    const int esz = c->dtype == DEFT_DTYPE_F32 ? 4 : 2;
+    const char* g = c->P.grads[0] + slot_base * esz;
+    cudaError_t e = launch_sgd_local(g, c->dtype, c->P.params[0], d_mom, 1, &offset, &numel,
+                                     &grad_scale, lr, momentum, s);
+    if (e != cudaSuccess) return cuda_fail(e, "sgd_local_kernel");
+    return DEFT_OK;
+  }
+  cudaError_t e = launch_update_allgather(c->P, c->rank, c->world, c->dtype, slot_base, offset,
+                                          numel, lr, momentum, grad_scale, d_mom, ++c->epoch_up,
+                                          s);
+  if (e != cudaSuccess) return cuda_fail(e, "update_allgather_kernel");
+  return DEFT_OK;
+}
+
+extern "C" deft_status_t deft_sgd_momentum_update(const void* d_grad, int32_t grad_dtype,
+                                                  float* d_param, float* d_mom, int64_t numel,
+                                                  float lr, float momentum, float grad_scale,
+                                                  void* stream) {
+  if (numel == 0) return DEFT_OK;
+  int64_t off = 0;
+  cudaError_t e = launch_sgd_local(d_grad, grad_dtype, d_param, d_mom, 1, &off, &numel,
+                                   &grad_scale, lr, momentum, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "sgd_local_kernel");
+  return DEFT_OK;
+}
+
+extern "C" deft_status_t deft_sgd_momentum_update_multi(const void* d_grad, int32_t grad_dtype,
+                                                        float* d_param, float* d_mom,
+                                                        int32_t count, const int64_t* offsets,
+                                                        const int64_t* numels,
+                                                        const float* grad_scales, float lr,
+                                                        float momentum, void* stream) {
+  if (count <= 0) return DEFT_OK;
+  cudaError_t e = launch_sgd_local(d_grad, grad_dtype, d_param, d_mom, count, offsets, numels,
+                                   grad_scales, lr, momentum, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "sgd_local_kernel");
+  return DEFT_OK;
+}

@@ -1,0 +1,85 @@
+// Shared declarations of the libdeft_b200 translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define DEFT_MAX_EXACT_CAPACITY_DEV 10000000LL  // knapsack.py:16
+
+namespace deft {
+
+// ---- launch accounting (deft_launch_count) --------------------------------
+void count_launch(uint64_t n = 1);
+
+// ---- K1 subset-sum --------------------------------------------------------
+struct SubsetSumLaunch {
+  const int64_t* weights;
+  const int32_t* item_off;
+  const int64_t* caps;
+  const int64_t* row_off;
+  const int64_t* meta_off;
+  uint32_t* rows;
+  int32_t* meta;
+  uint8_t* take;
+  int64_t* best;
+  const int32_t* pids_small;  // problems whose row fits in shared memory
+  int32_t n_small;
+  int64_t max_small_words;
+  const int32_t* pids_large;  // problems on the global-memory row path
+  int32_t n_large;
+};
+cudaError_t launch_subset_sum(const SubsetSumLaunch& L, cudaStream_t stream);
+int64_t host_scaled_cap(int64_t cap0);
+int64_t host_row_words(int64_t cap0);
+int64_t smem_words_limit();
+
+// ---- bucket communication + fused update ----------------------------------
+constexpr int kMaxWorld = 8;
+constexpr int kMaxCommBlocks = 256;
+// flag area layout (uint32): [kNumBarrierSets][kMaxCommBlocks][kMaxWorld]
+enum BarrierSet : int { kBarrierRS = 0, kBarrierCE = 1, kBarrierUpdate = 2, kNumBarrierSets = 3 };
+
+struct PeerPtrs {
+  char* grads[kMaxWorld];
+  float* params[kMaxWorld];
+  uint32_t* flags[kMaxWorld];
+};
+
+struct ShardRange {
+  int64_t lo, hi;  // absolute element range [lo, hi) of this rank's shard
+};
+
+// Absolute element shard [lo, hi) of rank `r` for bucket [offset, offset+numel):
+// interior boundaries are 16-byte aligned so the body can use 128-bit accesses.
+__host__ __device__ inline ShardRange shard_of(int64_t offset, int64_t numel, int r, int world,
+                                               int align_elems) {
+  const int64_t per = (numel + world - 1) / world;
+  auto bound = [&](int k) -> int64_t {
+    if (k <= 0) return offset;
+    if (k >= world) return offset + numel;
+    int64_t b = offset + (int64_t)k * per;
+    b = (b + align_elems - 1) / align_elems * align_elems;
+    return b < offset + numel ? b : offset + numel;
+  };
+  return ShardRange{bound(r), bound(r + 1)};
+}
+
+int comm_grid_for(int64_t elems_per_rank);
+
+cudaError_t launch_reduce_scatter_sm(const PeerPtrs& P, int rank, int world, int dtype,
+                                     int64_t slot_base, int64_t offset, int64_t numel,
+                                     uint32_t epoch, cudaStream_t stream);
+cudaError_t launch_barrier(const PeerPtrs& P, int rank, int world, int set, uint32_t epoch,
+                           cudaStream_t stream);
+cudaError_t launch_ce_reduce(char* own_grad_slot, const char* staging, int dtype, int world,
+                             int rank, int64_t shard_lo, int64_t shard_len,
+                             int64_t staging_stride_elems, cudaStream_t stream);
+cudaError_t launch_update_allgather(const PeerPtrs& P, int rank, int world, int dtype,
+                                    int64_t slot_base, int64_t offset, int64_t numel, float lr,
+                                    float momentum, float grad_scale, float* mom,
+                                    uint32_t epoch, cudaStream_t stream);
+cudaError_t launch_sgd_local(const void* grad, int dtype, float* param, float* mom,
+                             int32_t count, const int64_t* offsets, const int64_t* numels,
+                             const float* scales, float lr, float momentum,
+                             cudaStream_t stream);
+
+}  // namespace deft

@@ -1,0 +1,166 @@
+"""Host logic of the product (partition, greedy, state machine, preserver)
+against the reference's golden vectors -- on CPU.  The subset-sum DP is
+explicitly swapped for the C oracle here (the product default is the GPU
+kernel; tests/test_gpu_solver.py runs the same checks through it)."""
+import hashlib
+import json
+
+import pytest
+
+from conftest import GOLDEN, golden_schedule_text, read_jsonl_gz, spec_inputs
+from oracle import deft_oracle as O
+import paper_2503_16815_b200 as D
+from paper_2503_16815_b200 import knapsack as K
+
+
+@pytest.fixture(autouse=True)
+def oracle_dp():
+    with K.subset_sum_backend(O.subset_sum_c_batch):
+        yield
+
+
+def build_product_inputs(entry, inputs):
+    prof_d, cluster_d, part, bw, mult, iters = spec_inputs(entry, inputs)
+    prof = D.profile_from_dict(prof_d)
+    if bw != 1.0:
+        prof = prof.scaled_comm(1.0 / bw)
+    cluster = D.cluster_from_dict(cluster_d)
+    cfg = D.PartitionConfig(**part) if part else None
+    return prof, cluster, cfg, mult, iters
+
+
+def product_stream(entry, inputs) -> str:
+    prof, cluster, cfg, mult, iters = build_product_inputs(entry, inputs)
+    if cfg is None:
+        decisions = D.DeftScheduler(prof, cluster, mult).run(iters)
+        sched = D.Schedule("deft", prof, cluster, decisions, True, iters)
+    else:
+        sched = D.deft_schedule(prof, cluster, cfg, iters,
+                                single_link=entry["spec"].get("single_link", False))
+    return "".join(l + "\n" for l in sched.jsonl_lines())
+
+
+def test_naive_knapsack_golden():
+    for r in read_jsonl_gz("naive.jsonl.gz"):
+        items = [D.Item(i, w) for i, w in zip(r["ids"], r["weights"])]
+        asn = D.naive_knapsack(items, r["cap"])
+        assert asn.selections == (tuple(r["selection"]),)
+        assert asn.total_value == r["value"]
+        assert asn.leftovers == tuple(r["leftovers"])
+
+
+def test_recursive_knapsack_golden():
+    for r in read_jsonl_gz("recursive.jsonl.gz"):
+        items = [D.Item(i, w) for i, w in zip(r["ids"], r["weights"])]
+        assert D.recursive_knapsack(items, r["remain"], r["backward"]) == r["order"], r
+
+
+def test_greedy_golden():
+    for r in read_jsonl_gz("greedy.jsonl.gz"):
+        items = [D.Item(i, w) for i, w in enumerate(r["weights"], 1)]
+        asn = D.greedy_multi_knapsack(items, r["caps"])
+        assert [list(s) for s in asn.selections] == r["selections"]
+        assert asn.total_value == r["value"]
+        assert list(asn.leftovers) == r["leftovers"]
+
+
+def test_errors_mirror_reference():
+    with pytest.raises(D.DeftError):
+        D.Item(1, 0)
+    with pytest.raises(D.DeftError):
+        D.naive_knapsack([D.Item(1, 1)], -1)
+    with pytest.raises(D.DeftError):
+        D.recursive_knapsack([D.Item(1, 1)], 5, [])
+    with pytest.raises(D.DeftError):
+        D.greedy_multi_knapsack([], [-1])
+    with pytest.raises(D.DeftError, match="at most 20"):
+        D.brute_force_multi_knapsack([D.Item(i, 1) for i in range(1, 22)], [5])
+    assert D.naive_knapsack([], 10).selections == ((),)
+
+
+def test_partition_golden(golden_inputs):
+    for row in json.loads((GOLDEN / "partition.json").read_text()):
+        pname, cname, bw = row["key"].split("__")
+        bw = float(bw[2:])
+        prof = D.profile_from_dict(golden_inputs["profiles"][pname])
+        if bw != 1.0:
+            prof = prof.scaled_comm(1.0 / bw)
+        mu = {"dual": 1.65, "fast": 1.0, "equal_dual": 1.0}[cname]
+        cfg = D.PartitionConfig(partition_size=6_500_000, mu=mu)
+        if row.get("infeasible"):
+            with pytest.raises(D.InfeasiblePartitionError):
+                D.partition_buckets(prof, cfg)
+            continue
+        got = D.profile_to_dict(D.partition_buckets(prof, cfg))["buckets"]
+        assert got == row["buckets"]
+
+
+def test_product_schedules_match_reference(golden_index, golden_inputs):
+    n = 0
+    for e in golden_index:
+        if len(e["partitioned"]) > 200:
+            continue  # the 551-bucket sweep point runs on the GPU test only
+        text = product_stream(e, golden_inputs)
+        assert hashlib.sha256(text.encode()).hexdigest() == e["sha256"], e["key"]
+        assert text == golden_schedule_text(e)
+        n += 1
+    assert n >= 50
+
+
+def test_exec_notes_are_consistent(golden_index, golden_inputs):
+    """Every planned transfer carries a group; groups drain exactly once and in
+    origin order; merges accumulate into the live future group."""
+    for e in golden_index[:40]:
+        prof, cluster, cfg, mult, iters = build_product_inputs(e, golden_inputs)
+        if cfg is None:
+            continue
+        sched = D.deft_schedule(prof, cluster, cfg, iters)
+        sent: dict[int, list[int]] = {}
+        drained = []
+        for d in sched.decisions:
+            plan_ids = sorted(i for ids in d.plan().values() for i in ids)
+            assert sorted(t.bucket_id for t in d.exec.transfers) == plan_ids
+            for t in d.exec.transfers:
+                assert t.group >= 0
+                sent.setdefault(t.group, []).append(t.bucket_id)
+                assert t.fresh == (t.bucket_id in d.fresh_ids) or not t.fresh
+            for uid, k, origins in d.exec.updates:
+                assert sorted(sent.pop(uid)) == list(range(1, sched.profile.n_buckets + 1))
+                drained.append(origins)
+            assert [(u.origins, u.merge_count) for u in d.update_events] == \
+                [(o, k) for _, k, o in d.exec.updates]
+        flat = [o for origins in drained for o in origins]
+        assert flat == sorted(flat) and len(flat) == len(set(flat))
+
+
+def test_feedback_loop_golden(golden_index, golden_inputs):
+    walk = D.WalkParams.from_dict(golden_inputs["walk"])
+    checked = 0
+    for e in golden_index:
+        v = e.get("verdict")
+        if v is None or len(e["partitioned"]) > 40:
+            continue
+        prof, cluster, cfg, _, iters = build_product_inputs(e, golden_inputs)
+        for speculate in (True, False) if checked < 3 else (True,):
+            sched, got = D.feedback_loop(prof, cluster, cfg, walk, iterations=iters,
+                                         speculate=speculate)
+            text = "".join(l + "\n" for l in sched.jsonl_lines())
+            assert hashlib.sha256(text.encode()).hexdigest() == v["final_sha256"], e["key"]
+            assert got.preserved == v["preserved"]
+            assert got.retries == v["retries"]
+            assert got.capacity_multiplier == v["capacity_multiplier"]
+            assert got.ratio == v["ratio"]
+            assert list(got.sequence.k_values) == v["k_values"]
+        checked += 1
+    assert checked >= 20
+
+
+def test_preserver_golden(golden_inputs):
+    walk = D.WalkParams.from_dict(golden_inputs["walk"])
+    for row in json.loads((GOLDEN / "preserver.json").read_text()):
+        if row["kind"] == "next":
+            assert D.expected_next_state(row["s"], row["batch"], walk) == row["value"]
+        else:
+            seq = D.BatchSequence(tuple(row["k_values"]), row["batch"])
+            assert D.check_sequence(seq, walk) == (row["preserved"], row["ratio"],
+                                                   row["merged"], row["base"])
