@@ -1,0 +1,379 @@
+"""DeFT delayed-update data-parallel training step on B200s.
+
+python bench.py [--gpus N --steps K --warmup W --model resnet101|vgg19|gpt2]
+    [--impl deft|reference]
+
+A step = one DeFT-scheduled training iteration (forward, backward, bucket
+reduce-scatter on the schedule's NVLink channels, fused delayed SGD/momentum
+update + parameter all-gather) of the named model on synthetic data,
+batch 64 per GPU (BASELINE.json configs[1]: ResNet-101, 224x224).
+Under torchrun (N > 1) every rank runs one GPU; rank 0 prints ONE JSON line.
+
+--impl reference runs the CPU path (the oracle port of the reference's
+scheduler plus the delayed-SGD oracle, oracle/), rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BATCH = 64
+METRIC = "samples/sec (DeFT delayed-update DP training step)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--model", default="resnet101", choices=["resnet101", "vgg19", "gpt2"])
+    ap.add_argument("--impl", default="deft", choices=["deft", "reference"])
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "src": "measured"}
+    return {"hbm_gbs": 6650.0, "src": "fallback"}
+
+
+# ----------------------------------------------------------------- workloads
+
+def build_model(name, device):
+    import torch
+    import torchvision
+    torch.manual_seed(0)
+    if name == "resnet101":
+        m = torchvision.models.resnet101()
+    elif name == "vgg19":
+        m = torchvision.models.vgg19()
+    else:
+        from transformers import GPT2Config, GPT2LMHeadModel
+        m = GPT2LMHeadModel(GPT2Config(n_positions=1024))
+    m = m.to(device)
+    if name != "gpt2":
+        m = m.to(memory_format=torch.channels_last)
+    return m
+
+
+def make_batch(name, batch, device, seed=1234):
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    if name == "gpt2":
+        x = torch.randint(0, 50257, (batch, 1024), generator=g)
+        return (x.to(device), x.to(device))
+    x = torch.randn(batch, 3, 224, 224, generator=g)
+    y = torch.randint(0, 1000, (batch,), generator=g)
+    if device != "cpu":
+        x = x.to(device).contiguous(memory_format=torch.channels_last)
+        y = y.to(device)
+    return (x, y)
+
+
+def loss_fn_for(name):
+    import torch.nn.functional as F
+
+    if name == "gpt2":
+        def loss_fn(module, batch):
+            out = module(batch[0], labels=batch[1])
+            return out.loss
+    else:
+        def loss_fn(module, batch):
+            return F.cross_entropy(module(batch[0]), batch[1])
+    return loss_fn
+
+
+# ----------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:6]) if v == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- CPU path
+
+def cpu_reference_run(model_name, steps, warmup, batch):
+    """The reference's CPU path (oracle port): the DeFT decision stream from the
+    oracle scheduler on the fixture profile, CPU fwd/bwd, delayed SGD/momentum
+    exactly as oracle/delayed_sgd.py.  Bounded sample: `batch` samples/step."""
+    import torch
+    from oracle import deft_oracle as O
+
+    inputs = json.loads((ROOT / "tests" / "golden" / "inputs.json").read_text())
+    prof = inputs["profiles"]["resnet101" if model_name != "gpt2" else "gpt2"]
+    cl = inputs["clusters"]["dual"]
+    part = O.partition(prof["buckets"], sum(b["forward_us"] for b in prof["buckets"]),
+                       6_500_000, 1.65)
+    torch.set_num_threads(os.cpu_count() or 1)
+    model = build_model(model_name, "cpu")
+    params = [p for p in model.parameters() if p.requires_grad][::-1]
+    loss_fn = loss_fn_for(model_name)
+    data = make_batch(model_name, batch, "cpu")
+    total = sum(p.numel() for p in params)
+    v = torch.zeros(total)
+    summed = {}
+    n = warmup + steps
+    t_sched0 = time.perf_counter()
+    decisions = O.schedule(part, [l["speed_ratio_to_fast"] for l in cl["links"]],
+                           [l["name"] for l in cl["links"]], n + 2)
+    t_sched = time.perf_counter() - t_sched0
+    events = {d["iteration"]: d["update_events"] for d in decisions if d["stage"] == "backward"}
+    t0 = None
+    for s in range(n):
+        if s == warmup:
+            t0 = time.perf_counter()
+        flat = torch.cat([p.detach().reshape(-1) for p in params])
+        for u in events.get(s - 2, ()):
+            g = sum(summed.pop(o) for o in u["origins"]) / u["merge_count"]
+            v.mul_(0.9).add_(g)
+            flat.add_(v, alpha=-0.1)
+        off = 0
+        with torch.no_grad():
+            for p in params:
+                p.copy_(flat[off:off + p.numel()].view_as(p))
+                off += p.numel()
+        for p in params:
+            p.grad = None
+        loss = loss_fn(model, data)
+        loss.backward()
+        summed[s] = torch.cat([p.grad.reshape(-1) for p in params])
+    dt = time.perf_counter() - t0
+    return {"value": steps * batch / dt, "unit": "samples/s", "cores": torch.get_num_threads(),
+            "kind": "port",
+            "sample": f"{model_name} fp32 CPU fwd+bwd, batch {batch} x {steps} timed steps "
+                      f"(+{warmup} warm-up), oracle DeFT schedule (dual link, 6.5M partition, "
+                      f"{t_sched * 1e3:.0f} ms for {n + 2} iterations) + oracle delayed "
+                      f"SGD/momentum"}
+
+
+# ----------------------------------------------------------------- GPU path
+
+def main():
+    args = parse()
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = cpu_reference_run(args.model, max(1, min(args.steps, 3)), 1, 4)
+        line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": "samples/s",
+                "n_gpus": args.gpus, "steps": max(1, min(args.steps, 3)), "warmup": 1,
+                "ms_per_step": 4 / r["value"] * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"{args.model} DeFT delayed-update DP (CPU path)",
+                           "global_batch": 4, "note": "bounded CPU sample of configs[1]"},
+                "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": r["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    torch.backends.cudnn.benchmark = True
+    import paper_2503_16815_b200 as D
+    from paper_2503_16815_b200 import _native
+
+    model = build_model(args.model, device)
+    walk = D.WalkParams.from_dict(
+        json.loads((ROOT / "tests" / "golden" / "inputs.json").read_text())["walk"])
+    cfg = D.DeftConfig(lr=0.1, momentum=0.9, walk=walk,
+                       partition=D.PartitionConfig(partition_size=6_500_000, mu=1.0))
+    ddp = D.DeftDataParallel(model, cfg)
+    loss_fn = loss_fn_for(args.model)
+    batch = make_batch(args.model, args.batch, device, seed=1234 + rank)
+
+    # compute-only reference (no DeFT machinery): fwd + bwd into .grad
+    def plain_step():
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = loss_fn(model, batch)
+        loss.backward()
+        return loss
+
+    t_setup = time.perf_counter()
+    prof = ddp.measure_profile(batch, loss_fn, iters=3, name=args.model, batch_size=args.batch)
+    part = ddp.plan()
+    t_setup = time.perf_counter() - t_setup
+
+    def timed(step_fn, k):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(k):
+            step_fn()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([ms], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(args.warmup):
+        ddp.train_step(batch, loss_fn)
+    n0 = _native.launch_count()
+    with ClockSampler(local) as clk:
+        ms = timed(lambda: ddp.train_step(batch, loss_fn), args.steps)
+    launches = _native.launch_count() - n0
+    ms_step = ms / args.steps
+    value = args.batch * world * args.steps / (ms / 1e3)
+
+    # e2e: inputs from pinned host memory each step, loss read back each step
+    hx = batch[0].cpu().pin_memory()
+    hy = batch[1].cpu().pin_memory()
+    loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
+    dx, dy = torch.empty_like(batch[0]), torch.empty_like(batch[1])
+
+    def e2e_step():
+        dx.copy_(hx, non_blocking=True)
+        dy.copy_(hy, non_blocking=True)
+        loss = ddp.train_step((dx, dy), loss_fn)
+        loss_host.copy_(loss.detach().float().reshape(1), non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    ms_e2e = timed(e2e_step, args.steps)
+    e2e_value = args.batch * world * args.steps / (ms_e2e / 1e3)
+    h2d = hx.numel() * hx.element_size() + hy.numel() * hy.element_size()
+
+    # kernel roofline: instrumented pass (CUDA events around every native launch,
+    # on the stream each kernel is launched on)
+    ddp.cfg.instrument = True
+    ddp.timing_summary()
+    timed(lambda: ddp.train_step(batch, loss_fn), max(3, args.steps // 2))
+    ks = ddp.timing_summary()
+    ddp.cfg.instrument = False
+
+    # compute-only step time (for exposed comm): same model, plain fwd+bwd
+    for p in model.parameters():
+        p.grad = None
+    saved = ddp._bound_slot
+    for _ in range(2):
+        plain_step()
+        for p in model.parameters():
+            p.grad = None
+    ms_plain = timed(lambda: (plain_step(), [setattr(p, "grad", None)
+                                             for p in model.parameters()]), args.steps)
+    ddp._bound_slot = None
+    if saved is not None:
+        ddp._bind_grads(saved)
+
+    pk = peaks()
+    dom = max(ks.items(), key=lambda kv: kv[1]["ms"]) if ks else None
+    roof = None
+    if dom:
+        kind, r = dom
+        avg_ms = r["ms"] / r["launches"]
+        achieved = (r["bytes"] / r["launches"]) / (avg_ms / 1e3) / 1e9
+        peak = pk["hbm_gbs"] if (kind == "update" and world == 1) else 770.0
+        roof = {"kernel": {"update": "sgd_local_kernel" if world == 1 else
+                           "update_allgather_kernel",
+                           "reduce_scatter": "reduce_scatter_kernel"}[kind],
+                "bound": "hbm" if (kind == "update" and world == 1) else "nvlink",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "launches_per_step": round(r["launches"] / max(3, args.steps // 2), 2),
+                "avg_launch_us": round(avg_ms * 1e3, 2),
+                "bytes_per_launch": int(r["bytes"] / r["launches"]),
+                "peak_src": pk["src"] if peak != 770.0 else "guide: measured peer copy 770 GB/s",
+                "all_kernels": ks}
+
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu_base = cpu_reference_run(args.model, 2, 1, 4)
+        except Exception as e:  # reported, never fatal
+            cpu_base = {"error": repr(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, randn images / random tokens)",
+            "config": {"workload": f"{args.model} DeFT delayed-update DP, batch "
+                                   f"{args.batch}/GPU" + (", 224x224" if args.model != "gpt2"
+                                                           else ", seq 1024"),
+                       "model": args.model, "global_batch": args.batch * world,
+                       "parallelism": f"dp{world}", "l2": "working set (activations) >> L2 126 MB",
+                       "grad_dtype": "fp32", "compute": "bf16 autocast",
+                       "buckets": part.n_buckets, "links": [l.name for l in ddp.cluster.links],
+                       "capacity_multiplier": ddp.capacity_multiplier,
+                       "setup_s": round(t_setup, 2)},
+            "e2e": {"value": round(e2e_value, 2), "unit": "samples/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4},
+            "gpu_launches": int(launches),
+            "exposed_comm_ms": round(ms_step - ms_plain / args.steps, 3),
+            "compute_only_ms_per_step": round(ms_plain / args.steps, 3),
+            "roofline": roof,
+            "cpu_baseline": cpu_base,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    ddp.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,139 @@
+"""Symmetric device memory and the bucket communicator (one process per GPU).
+
+Each rank cudaMalloc's its gradient arena, parameter buffer and barrier flags
+inside libdeft_b200.so, exports CUDA IPC handles, exchanges them through
+``torch.distributed`` (plumbing only -- no collective touches the data path)
+and maps every peer's buffers.  The kernels then read peers' gradient slots and
+write peers' parameters directly over NVLink / NVSwitch.
+
+This replaces the reference's abstract links (profiles.py:18-40; durations
+simulator.py:136-147): link 0 / "fast" is the SM-driven P2P channel, the
+second link is the copy-engine channel.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _native
+from ._native import CHANNEL_CE, CHANNEL_SM, DTYPE_BF16, DTYPE_F32, IPC_HANDLE_BYTES, c_vp, check
+
+_TYPESTR = {torch.float32: "<f4", torch.bfloat16: "<i2", torch.uint8: "|u1"}
+
+
+class _Region:
+    """A raw device allocation exposed through __cuda_array_interface__ so that
+    torch.as_tensor wraps it without a copy.  Freed when the last tensor dies."""
+
+    def __init__(self, nbytes: int, ipc: bool):
+        self.ptr = c_vp()
+        self.nbytes = nbytes
+        self.handle = (ctypes.c_uint8 * IPC_HANDLE_BYTES)() if ipc else None
+        check(_native.lib().deft_mem_alloc(nbytes, ctypes.byref(self.ptr), self.handle),
+              "deft_mem_alloc")
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (self.ptr.value, False), "version": 3}
+
+    def __del__(self):
+        if getattr(self, "ptr", None) is not None and self.ptr.value and _native._lib is not None:
+            _native.lib().deft_mem_free(self.ptr)
+            self.ptr = None
+
+
+def region_tensor(nbytes: int, dtype: torch.dtype, ipc: bool, device: torch.device):
+    reg = _Region(nbytes, ipc)
+    raw = torch.as_tensor(reg, device=device)  # uint8 view, keeps `reg` alive
+    if raw.data_ptr() != reg.ptr.value:
+        raise RuntimeError("torch.as_tensor copied the symmetric region")
+    t = raw.view(torch.int16 if dtype == torch.bfloat16 else dtype)
+    return (t.view(torch.bfloat16) if dtype == torch.bfloat16 else t), reg
+
+
+@dataclass
+class PeerMaps:
+    grads: list[int]
+    params: list[int]
+    flags: list[int]
+
+
+class BucketComm:
+    """Per-rank communicator over the symmetric gradient arena / params / flags."""
+
+    def __init__(self, rank: int, world: int, n_slots: int, slot_elems: int,
+                 grad_dtype: torch.dtype, device: torch.device, group=None):
+        self.rank, self.world = rank, world
+        self.n_slots, self.slot_elems = n_slots, slot_elems
+        self.grad_dtype = grad_dtype
+        self.device = device
+        esz = 2 if grad_dtype == torch.bfloat16 else 4
+        ipc = world > 1
+        self.grads, self._g = region_tensor(n_slots * slot_elems * esz, grad_dtype, ipc, device)
+        self.grads = self.grads.view(n_slots, slot_elems)
+        self.params, self._p = region_tensor(slot_elems * 4, torch.float32, ipc, device)
+        fbytes = int(_native.lib().deft_comm_flag_bytes(world))
+        self.flags, self._f = region_tensor(fbytes, torch.uint8, ipc, device)
+        self._opened: list[c_vp] = []
+        if world > 1:
+            maps = self._exchange(group)
+        else:
+            maps = PeerMaps([self._g.ptr.value], [self._p.ptr.value], [self._f.ptr.value])
+        arr = lambda xs: (c_vp * world)(*xs)  # noqa: E731
+        h = c_vp()
+        check(_native.lib().deft_comm_create(
+            rank, world, arr(maps.grads), arr(maps.params), arr(maps.flags), slot_elems, n_slots,
+            DTYPE_BF16 if grad_dtype == torch.bfloat16 else DTYPE_F32, ctypes.byref(h)),
+            "deft_comm_create")
+        self._h = h
+
+    def _exchange(self, group) -> PeerMaps:
+        import torch.distributed as dist
+        mine = [bytes(r.handle) for r in (self._g, self._p, self._f)]
+        allh: list = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        out = PeerMaps([], [], [])
+        for r in range(self.world):
+            if r == self.rank:
+                out.grads.append(self._g.ptr.value)
+                out.params.append(self._p.ptr.value)
+                out.flags.append(self._f.ptr.value)
+                continue
+            for lst, hbytes in zip((out.grads, out.params, out.flags), allh[r]):
+                p = c_vp()
+                hb = (ctypes.c_uint8 * IPC_HANDLE_BYTES).from_buffer_copy(hbytes)
+                check(_native.lib().deft_mem_open(hb, ctypes.byref(p)), "deft_mem_open")
+                self._opened.append(p)
+                lst.append(p.value)
+        dist.barrier(group=group)
+        return out
+
+    def reduce_scatter(self, channel: int, slot: int, offset: int, numel: int, stream) -> None:
+        check(_native.lib().deft_bucket_reduce_scatter(self._h, channel, slot, offset, numel,
+                                                       c_vp(stream.cuda_stream)),
+              "deft_bucket_reduce_scatter")
+
+    def update(self, slot: int, offset: int, numel: int, lr: float, momentum: float,
+               grad_scale: float, mom: torch.Tensor, stream) -> None:
+        check(_native.lib().deft_bucket_update(self._h, slot, offset, numel, lr, momentum,
+                                               grad_scale, c_vp(mom.data_ptr()),
+                                               c_vp(stream.cuda_stream)),
+              "deft_bucket_update")
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None:
+            torch.cuda.synchronize(self.device)
+            _native.lib().deft_comm_destroy(self._h)
+            self._h = None
+            for p in self._opened:
+                _native.lib().deft_mem_close(p)
+            self._opened = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+__all__ = ["BucketComm", "region_tensor", "CHANNEL_SM", "CHANNEL_CE"]

@@ -1,0 +1,517 @@
+"""DeftDataParallel: runs a DeFT decision stream on real GPUs.
+
+The reference plays decisions onto a simulated timeline (simulator.py:150-273);
+this executor plays them onto CUDA streams with the same release rules
+(simulator.py:184-196):
+
+  * forward-plan transfers are released at the forward-stage start;
+  * backward-plan transfers of older groups at the backward-stage start;
+  * fresh transfers at their own bucket's backward end (a post-accumulate-grad
+    hook records the event and launches the reduce on the link's stream).
+
+Channels: link i of the ClusterSpec maps to an NVLink channel (SM P2P or copy
+engines); every link owns one CUDA stream, so a link serves its transfers in
+release order like the simulator's per-link queue (simulator.py:94-133).
+
+Delayed update (stale-by-k, SURVEY §8c rule 4).  Update events carried by
+decision (t, backward) are applied -- per bucket, fused with the parameter
+all-gather -- inside bucket b's no-read window of iteration t+1 (after its
+backward, before its next forward) and are therefore visible from iteration
+t+2 on, deterministically, whatever the communication timing:
+    theta^(s) = theta^(s-1) - lr * v,   v = m*v + sum_{o in origins} mean_ranks(g_o) / k
+for every event of decision (s-2, backward).  Compute never waits for a
+transfer; it only waits, at each forward start, for the (short) update
+kernels due at that version -- the zero-stall property of simulator.py:12-14.
+
+Memory (B200, 180 GB HBM): the flat fp32 parameter buffer (output-side
+bucket first, every module parameter is a view into it), a momentum buffer
+and ``n_slots`` gradient group slots, all symmetric (CUDA-IPC mapped by every
+peer).  Autograd accumulates straight into the slot of the group the schedule
+says this iteration's gradients join (store -> zeroed slot, merge -> the live
+future group's slot), so merging k iterations is plain gradient accumulation
+ with no extra pass.
+"""
+from __future__ import annotations
+
+import math
+from collections import defaultdict
+from dataclasses import dataclass, field
+from typing import Callable
+
+import torch
+
+from . import _native
+from .comm import BucketComm
+from .errors import DeftError, InternalInvariantError
+from .partition import PartitionConfig, element_ranges, partition_buckets
+from .preserver import WalkParams, feedback_loop
+from .profiles import BucketProfile, ClusterSpec, LinkSpec, ModelProfile
+from .scheduler import DeftScheduler, ScheduleDecision
+
+
+@dataclass
+class DeftConfig:
+    lr: float = 0.1
+    momentum: float = 0.9
+    partition: PartitionConfig = field(default_factory=PartitionConfig)
+    grad_dtype: torch.dtype = torch.float32
+    n_slots: int = 5
+    autocast_dtype: torch.dtype | None = torch.bfloat16
+    walk: WalkParams | None = None          # run the feedback loop when given
+    capacity_multiplier: float = 1.0
+    lookahead: int = 32                     # decisions generated ahead of execution
+    use_ce_channel: bool = True             # second link = copy engines
+    instrument: bool = False                # CUDA events around every native launch
+
+
+class _Bucket:
+    __slots__ = ("id", "lo", "hi", "params")
+
+    def __init__(self, bid, lo, hi):
+        self.id, self.lo, self.hi, self.params = bid, lo, hi, []
+
+
+class DeftDataParallel:
+    """Wraps a module; ``train_step`` runs one DeFT-scheduled iteration."""
+
+    def __init__(self, module: torch.nn.Module, config: DeftConfig | None = None,
+                 process_group=None, device: torch.device | None = None):
+        self.cfg = config or DeftConfig()
+        self.module = module
+        self.group = process_group
+        dist = torch.distributed
+        self.world = dist.get_world_size(process_group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(process_group) if dist.is_initialized() else 0
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        if self.device.type != "cuda":
+            raise DeftError("DeftDataParallel runs on CUDA devices only (no CPU fallback)")
+        # DDP order: output-side parameter first (bucket 1 finishes backward first)
+        self.params = [p for p in module.parameters() if p.requires_grad][::-1]
+        self.numels = [p.numel() for p in self.params]
+        self.total = sum(self.numels)
+        self.comm = BucketComm(self.rank, self.world, self.cfg.n_slots, self.total,
+                               self.cfg.grad_dtype, self.device, process_group)
+        self.mom = torch.zeros(self.total, dtype=torch.float32, device=self.device)
+        self._bind_params()
+        self.compute = torch.cuda.current_stream(self.device)
+        prio_lo, prio_hi = torch.cuda.Stream.priority_range()
+        self.update_stream = torch.cuda.Stream(self.device, priority=prio_hi)
+        self.link_streams: list[torch.cuda.Stream] = []
+        self.profile: ModelProfile | None = None
+        self.schedule_profile: ModelProfile | None = None
+        self.cluster: ClusterSpec | None = None
+        self.iteration = 0
+        self._events_t: list[tuple[str, torch.cuda.Event, torch.cuda.Event, int]] = []
+
+    # ------------------------------------------------------------------ setup
+
+    def _bind_params(self):
+        """Move every parameter into the symmetric flat buffer (same strides)."""
+        flat = self.comm.params
+        self.offsets = []
+        off = 0
+        with torch.no_grad():
+            for p in self.params:
+                n = p.numel()
+                view = flat[off:off + n].as_strided(p.shape, p.stride())
+                if not p.is_contiguous(memory_format=torch.contiguous_format) and \
+                        not p.is_contiguous(memory_format=torch.channels_last):
+                    raise DeftError("parameters must be dense (contiguous or channels_last)")
+                view.copy_(p.detach())
+                p.data = view
+                self.offsets.append(off)
+                off += n
+            if self.world > 1:
+                torch.distributed.broadcast(flat, src=0, group=self.group)
+        torch.cuda.synchronize(self.device)
+        self._grad_views = []
+        for s in range(self.cfg.n_slots):
+            row = self.comm.grads[s]
+            self._grad_views.append([row[o:o + p.numel()].as_strided(p.shape, p.stride())
+                                     for o, p in zip(self.offsets, self.params)])
+        self._bound_slot = None
+
+    def initial_buckets(self) -> list[tuple[int, int]]:
+        """Consecutive output-side-first tensors packed up to partition_size
+        parameters (larger tensors alone; partition_buckets splits them)."""
+        cap = self.cfg.partition.partition_size
+        out, lo, cur = [], 0, 0
+        for n in self.numels:
+            if cur and cur + n > cap:
+                out.append((lo, lo + cur))
+                lo, cur = lo + cur, 0
+            cur += n
+        if cur:
+            out.append((lo, lo + cur))
+        return out
+
+    # -------------------------------------------------------------- profiling
+
+    def _make_links(self, ce_ratio: float | None) -> ClusterSpec:
+        links = [LinkSpec("nvlink_sm", 1.0)]
+        self.channel_of_link = [_native.CHANNEL_SM]
+        if ce_ratio is not None:
+            if ce_ratio >= 1.0:
+                links.append(LinkSpec("nvlink_ce", ce_ratio))
+                self.channel_of_link.append(_native.CHANNEL_CE)
+            else:  # copy engines faster: they become the fast link
+                links = [LinkSpec("nvlink_ce", 1.0), LinkSpec("nvlink_sm", 1.0 / ce_ratio)]
+                self.channel_of_link = [_native.CHANNEL_CE, _native.CHANNEL_SM]
+        return ClusterSpec(links=tuple(links))
+
+    def measure_profile(self, batch, loss_fn: Callable, iters: int = 3, name: str = "model",
+                        batch_size: int = 1) -> ModelProfile:
+        """CUDA-event timing of forward/backward per initial bucket plus the
+        measured comm time of every bucket on each channel -> ModelProfile.
+        (B200 replacement of the paper's Nsight profiler.)"""
+        ranges = self.initial_buckets()
+        owner = self._owner_map(ranges)
+        fwd_ms = [0.0] * len(ranges)
+        bwd_ms = [0.0] * len(ranges)
+        module_first = {}
+        for m in self.module.modules():
+            ps = [p for p in m.parameters(recurse=False) if p.requires_grad]
+            if ps:
+                module_first[m] = max(max(owner[id(p)]) for p in ps)
+        for _ in range(iters + 1):
+            starts: dict[int, torch.cuda.Event] = {}
+            hooks = []
+
+            def pre(mod, _inp, b=None):
+                b = module_first[mod]
+                if b not in starts:
+                    e = torch.cuda.Event(enable_timing=True)
+                    e.record()
+                    starts[b] = e
+            for m in module_first:
+                hooks.append(m.register_forward_pre_hook(pre))
+            done: dict[int, torch.cuda.Event] = {}
+            pending = [len([p for p in self.params if b in owner[id(p)]])
+                       for b in range(len(ranges))]
+
+            def acc(p):
+                for b in owner[id(p)]:
+                    pending[b] -= 1
+                    if pending[b] == 0:
+                        e = torch.cuda.Event(enable_timing=True)
+                        e.record()
+                        done[b] = e
+            for p in self.params:
+                hooks.append(p.register_post_accumulate_grad_hook(acc))
+            self._bind_grads(0)
+            self.comm.grads[0].zero_()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            with self._autocast():
+                loss = loss_fn(self.module, batch)
+            ev1.record()
+            loss.backward()
+            ev2 = torch.cuda.Event(enable_timing=True)
+            ev2.record()
+            for h in hooks:
+                h.remove()
+            torch.cuda.synchronize(self.device)
+            if _ == 0:
+                continue  # warm-up
+            # forward: bucket n first; bucket b spans start[b] .. start[b-1]
+            nb = len(ranges)
+            marks = {b: ev0.elapsed_time(starts[b]) for b in starts}
+            prev_t = ev0.elapsed_time(ev1)
+            for b in range(nb):  # b = 0 is bucket 1 (output side)
+                t0 = marks.get(b, prev_t)
+                fwd_ms[b] += max(0.0, prev_t - t0) / iters
+                prev_t = min(prev_t, t0)
+            fwd_ms[nb - 1] += max(0.0, prev_t) / iters  # pre-module prologue -> input bucket
+            prev_t = ev0.elapsed_time(ev1)
+            for b in range(nb):
+                t1 = ev0.elapsed_time(done[b]) if b in done else ev0.elapsed_time(ev2)
+                bwd_ms[b] += max(0.0, t1 - prev_t) / iters
+                prev_t = max(prev_t, t1)
+        comm_sm = self._measure_comm(ranges, _native.CHANNEL_SM)
+        ce_ratio = None
+        if self.world > 1 and self.cfg.use_ce_channel:
+            comm_ce = self._measure_comm(ranges, _native.CHANNEL_CE)
+            ratios = sorted(c / s for c, s in zip(comm_ce, comm_sm) if s > 0)
+            ce_ratio = ratios[len(ratios) // 2] if ratios else None
+        if self.world > 1:  # every rank must plan the SAME schedule: rank 0's numbers win
+            obj = [(fwd_ms, bwd_ms, comm_sm, ce_ratio)]
+            torch.distributed.broadcast_object_list(obj, src=0, group=self.group)
+            fwd_ms, bwd_ms, comm_sm, ce_ratio = obj[0]
+        buckets = tuple(
+            BucketProfile(i + 1, hi - lo, max(0, round(fwd_ms[i] * 1000)),
+                          max(0, round(bwd_ms[i] * 1000)), max(1, round(comm_sm[i] * 1000)))
+            for i, (lo, hi) in enumerate(ranges))
+        self.cluster = self._make_links(ce_ratio)
+        self.profile = ModelProfile(name=name, buckets=buckets, batch_size=batch_size,
+                                    learning_rate=self.cfg.lr,
+                                    notes={"device": torch.cuda.get_device_name(self.device),
+                                           "world": self.world})
+        return self.profile
+
+    def _owner_map(self, ranges):
+        owner = {}
+        for p, off in zip(self.params, self.offsets):
+            lo, hi = off, off + p.numel()
+            owner[id(p)] = [b for b, (a, z) in enumerate(ranges) if a < hi and lo < z]
+        return owner
+
+    def _measure_comm(self, ranges, channel, reps: int = 3) -> list[float]:
+        if self.world == 1:
+            return [0.0] * len(ranges)
+        s = torch.cuda.Stream(self.device)
+        out = []
+        torch.cuda.synchronize(self.device)
+        for lo, hi in ranges:
+            best = float("inf")
+            for _ in range(reps + 1):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                self.comm.reduce_scatter(channel, 0, lo, hi - lo, s)
+                b.record(s)
+                b.synchronize()
+                best = min(best, a.elapsed_time(b))
+            out.append(best)
+        self.comm.grads[0].zero_()
+        torch.cuda.synchronize(self.device)
+        return out
+
+    # ---------------------------------------------------------------- planning
+
+    def plan(self, profile: ModelProfile | None = None, cluster: ClusterSpec | None = None,
+             feedback_iterations: int = 200):
+        """Partition the profile, pick the capacity multiplier (feedback loop when
+        walk parameters are configured) and start the incremental scheduler."""
+        profile = profile or self.profile
+        cluster = cluster or self.cluster
+        if profile is None or cluster is None:
+            raise DeftError("measure_profile() or an explicit profile/cluster is required")
+        if cluster is not self.cluster:
+            self.cluster = cluster
+            self.channel_of_link = [_native.CHANNEL_SM if l.is_fast else _native.CHANNEL_CE
+                                    for l in cluster.links]
+        mult = self.cfg.capacity_multiplier
+        self.verdict = None
+        if self.cfg.walk is not None:
+            _, self.verdict = feedback_loop(profile, cluster, self.cfg.partition, self.cfg.walk,
+                                            iterations=feedback_iterations)
+            mult = self.verdict.capacity_multiplier
+        part = partition_buckets(profile, self.cfg.partition)
+        if part.total_param_count != self.total:
+            raise DeftError(f"profile covers {part.total_param_count} parameters, "
+                            f"model has {self.total}")
+        self.schedule_profile = part
+        self.buckets = [_Bucket(b.id, lo, hi) for b, (lo, hi) in
+                        zip(part.buckets, element_ranges(part, None))]
+        owner = self._owner_map([(b.lo, b.hi) for b in self.buckets])
+        self._param_buckets = [owner[id(p)] for p in self.params]
+        self._bucket_nparams = [0] * len(self.buckets)
+        for bl in self._param_buckets:
+            for b in bl:
+                self._bucket_nparams[b] += 1
+        self.scheduler = DeftScheduler(part, cluster, mult)
+        self.capacity_multiplier = mult
+        self._decisions: dict[int, tuple[ScheduleDecision, ScheduleDecision]] = {}
+        self._next_sched = 0
+        self.decision_log: list[tuple[ScheduleDecision, ScheduleDecision]] = []
+        self.link_streams = [torch.cuda.Stream(self.device) for _ in cluster.links]
+        # runtime state
+        self._slot_of: dict[int, int] = {}
+        self._slot_free = [None] * self.cfg.n_slots   # event: slot reusable
+        self._slot_busy = [False] * self.cfg.n_slots
+        self._rs_done: dict[tuple[int, int], torch.cuda.Event] = {}
+        self._group_left: dict[int, int] = {}
+        self._due_updates: list[tuple[int, int]] = []   # (group uid, merge_count)
+        self._version_ready: torch.cuda.Event | None = None
+        self._in_step = False
+        self._hooks = [p.register_post_accumulate_grad_hook(self._on_grad)
+                       for p in self.params]
+        return part
+
+    def decisions(self, t: int) -> tuple[ScheduleDecision, ScheduleDecision]:
+        while self._next_sched <= t + self.cfg.lookahead:
+            k = self._next_sched
+            self._decisions[k] = (self.scheduler.schedule_forward(k),
+                                  self.scheduler.schedule_backward(k))
+            self._next_sched += 1
+        if t in self._decisions:
+            return self._decisions[t]
+        return self.decision_log[t]
+
+    # ---------------------------------------------------------------- runtime
+
+    def _autocast(self):
+        if self.cfg.autocast_dtype is None:
+            return torch.autocast("cuda", enabled=False)
+        return torch.autocast("cuda", dtype=self.cfg.autocast_dtype)
+
+    def _bind_grads(self, slot: int):
+        if self._bound_slot == slot:
+            return
+        for p, g in zip(self.params, self._grad_views[slot]):
+            p.grad = g
+        self._bound_slot = slot
+
+    def _slot_for(self, uid: int) -> int:
+        s = self._slot_of.get(uid)
+        if s is not None:
+            return s
+        for cand in range(self.cfg.n_slots):
+            if not self._slot_busy[cand]:
+                self._slot_busy[cand] = True
+                self._slot_of[uid] = cand
+                self._group_left[uid] = len(self.buckets)
+                return cand
+        raise InternalInvariantError(
+            f"all {self.cfg.n_slots} gradient slots are held by live groups; raise n_slots")
+
+    def _timed(self, kind: str, stream, fn, nbytes: int):
+        if not self.cfg.instrument:
+            fn()
+            return
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        self._events_t.append((kind, a, b, nbytes))
+
+    def _issue_rs(self, tr, release: torch.cuda.Event):
+        if self.world == 1:
+            return
+        b = self.buckets[tr.bucket_id - 1]
+        s = self.link_streams[tr.link]
+        s.wait_event(release)
+        slot = self._slot_of[tr.group]
+        esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
+        nbytes = (b.hi - b.lo) * esz * (self.world - 1) // self.world * 2
+        self._timed("reduce_scatter", s,
+                    lambda: self.comm.reduce_scatter(self.channel_of_link[tr.link], slot, b.lo,
+                                                     b.hi - b.lo, s), nbytes)
+        ev = torch.cuda.Event()
+        ev.record(s)
+        self._rs_done[(tr.group, tr.bucket_id)] = ev
+
+    def _issue_update(self, uid: int, k: int, bidx: int, window_open: torch.cuda.Event):
+        b = self.buckets[bidx]
+        s = self.update_stream
+        s.wait_event(window_open)
+        rs = self._rs_done.pop((uid, b.id), None)
+        if rs is not None:
+            s.wait_event(rs)
+        slot = self._slot_of[uid]
+        esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
+        shard = (b.hi - b.lo + self.world - 1) // self.world
+        nbytes = shard * (esz + 4 * 4) + shard * 4 * (self.world - 1)
+        self._timed("update", s,
+                    lambda: self.comm.update(slot, b.lo, b.hi - b.lo, self.cfg.lr,
+                                             self.cfg.momentum, 1.0 / (self.world * k),
+                                             self.mom, s), nbytes)
+        self._group_left[uid] -= 1
+        if self._group_left[uid] == 0:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            slot = self._slot_of.pop(uid)
+            del self._group_left[uid]
+            self._slot_free[slot] = ev
+            self._slot_busy[slot] = False
+
+    def _on_grad(self, p):
+        if not self._in_step:
+            return
+        idx = self._param_index[id(p)]
+        for b in self._param_buckets[idx]:
+            self._pending[b] -= 1
+            if self._pending[b] == 0:
+                self._bucket_ready(b)
+
+    def _bucket_ready(self, bidx: int):
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        for tr in self._fresh.pop(bidx + 1, ()):
+            self._issue_rs(tr, ev)
+        for uid, k in self._due_updates:
+            self._issue_update(uid, k, bidx, ev)
+        self._fired[bidx] = True
+
+    def train_step(self, batch, loss_fn: Callable) -> torch.Tensor:
+        """One DeFT iteration: forward (Case 1 transfers released), backward
+        (Case 2/3/4 transfers, fresh ones per bucket), delayed updates."""
+        if not hasattr(self, "scheduler"):
+            raise DeftError("call plan() before train_step()")
+        if not hasattr(self, "_param_index"):
+            self._param_index = {id(p): i for i, p in enumerate(self.params)}
+        t = self.iteration
+        dF, dB = self.decisions(t)
+        self.decision_log.append(self._decisions.pop(t))
+        comp = torch.cuda.current_stream(self.device)
+        if self._version_ready is not None:
+            comp.wait_event(self._version_ready)   # theta^(t) complete
+        ev_fwd = torch.cuda.Event()
+        ev_fwd.record(comp)
+        for tr in dF.exec.transfers:
+            self._issue_rs(tr, ev_fwd)
+        with self._autocast():
+            loss = loss_fn(self.module, batch)
+        # backward stage: where do this iteration's gradients go?
+        uid = dB.exec.grad_group
+        if uid is None:
+            raise InternalInvariantError("backward decision without a gradient group")
+        new = uid not in self._slot_of
+        slot = self._slot_for(uid)
+        if new:
+            if dB.exec.grad_merge:
+                raise InternalInvariantError("merge into a group that has no slot")
+            if self._slot_free[slot] is not None:
+                comp.wait_event(self._slot_free[slot])
+            self.comm.grads[slot].zero_()
+        self._bind_grads(slot)
+        ev_bwd = torch.cuda.Event()
+        ev_bwd.record(comp)
+        self._fresh = defaultdict(list)
+        for tr in dB.exec.transfers:
+            if tr.fresh:
+                self._fresh[tr.bucket_id].append(tr)
+            else:
+                self._issue_rs(tr, ev_bwd)
+        self._pending = list(self._bucket_nparams)
+        self._fired = [False] * len(self.buckets)
+        self._in_step = True
+        try:
+            loss.backward()
+        finally:
+            self._in_step = False
+        for b in range(len(self.buckets)):      # buckets whose params got no gradient
+            if not self._fired[b]:
+                self._bucket_ready(b)
+        if self._fresh:
+            raise InternalInvariantError("fresh transfers left unreleased")
+        ev = torch.cuda.Event()
+        ev.record(self.update_stream)
+        self._version_ready = ev
+        # events of THIS decision are applied during the next backward (visible at t+2)
+        self._due_updates = [(u, k) for u, k, _ in dB.exec.updates]
+        self.iteration += 1
+        return loss
+
+    def finish(self):
+        """Drain every stream (the trailing in-flight groups stay unapplied, as
+        in the reference where unaccounted iterations are still in flight)."""
+        torch.cuda.synchronize(self.device)
+
+    def timing_summary(self) -> dict:
+        """Per-kind (count, total ms, bytes) of the instrumented launches."""
+        torch.cuda.synchronize(self.device)
+        out: dict[str, list[float]] = {}
+        for kind, a, b, nbytes in self._events_t:
+            r = out.setdefault(kind, [0, 0.0, 0])
+            r[0] += 1
+            r[1] += a.elapsed_time(b)
+            r[2] += nbytes
+        self._events_t = []
+        return {k: {"launches": int(v[0]), "ms": v[1], "bytes": int(v[2])} for k, v in out.items()}
+
+    def close(self):
+        for h in getattr(self, "_hooks", []):
+            h.remove()
+        self._hooks = []
+        self.comm.close()
