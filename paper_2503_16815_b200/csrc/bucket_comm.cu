@@ -51,6 +51,31 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
+// Rank-private epoch counters live right after the peer-written flag words:
+// counters[set][block].  Block b of every kernel in barrier set `set` runs in
+// the same order on every rank (one stream per set), so the counters advance in
+// lock-step without any host involvement -- which keeps the kernels replayable
+// inside CUDA graphs.
+__device__ __forceinline__ uint32_t* epoch_counter(const PeerPtrs& P, int rank, int set,
+                                                   int block) {
+  return P.flags[rank] + (int64_t)kNumBarrierSets * kMaxCommBlocks * kMaxWorld +
+         (int64_t)set * kMaxCommBlocks + block;
+}
+
+// Advance this block's epoch by `step`; returns the previous value (all threads).
+__device__ __forceinline__ uint32_t take_epochs(const PeerPtrs& P, int rank, int set,
+                                                uint32_t step) {
+  __shared__ uint32_t s_epoch;
+  if (threadIdx.x == 0) {
+    uint32_t* c = epoch_counter(P, rank, set, blockIdx.x);
+    const uint32_t e = *c;
+    *c = e + step;
+    s_epoch = e;
+  }
+  __syncthreads();
+  return s_epoch;
+}
+
 // Block-level barrier with the same-index block on every rank.
 __device__ __forceinline__ void peer_block_barrier(const PeerPtrs& P, int rank, int world,
                                                    int set, int block, uint32_t value) {
@@ -132,8 +157,9 @@ __device__ __forceinline__ Span split_span(int64_t lo, int64_t hi) {
 // ============================================================================
 template <typename T>
 __global__ void __launch_bounds__(kCommThreads) reduce_scatter_kernel(
-    PeerPtrs P, int rank, int world, int64_t slot_base, int64_t lo, int64_t hi, uint32_t epoch) {
+    PeerPtrs P, int rank, int world, int64_t slot_base, int64_t lo, int64_t hi) {
   using V = Vec<T>;
+  const uint32_t epoch = take_epochs(P, rank, kBarrierRS, 1u) + 1u;
   peer_block_barrier(P, rank, world, kBarrierRS, blockIdx.x, epoch);
   const T* src[kMaxWorld];
 #pragma unroll
@@ -190,16 +216,16 @@ __global__ void __launch_bounds__(kCommThreads) reduce_scatter_kernel(
 
 cudaError_t launch_reduce_scatter_sm(const PeerPtrs& P, int rank, int world, int dtype,
                                      int64_t slot_base, int64_t offset, int64_t numel,
-                                     uint32_t epoch, cudaStream_t stream) {
+                                     cudaStream_t stream) {
   const int align = dtype == 0 ? 4 : 8;
   const ShardRange sh = shard_of(offset, numel, rank, world, align);
   const int grid = comm_grid_for((numel + world - 1) / world);
   if (dtype == 0)
     reduce_scatter_kernel<float><<<grid, kCommThreads, 0, stream>>>(P, rank, world, slot_base,
-                                                                   sh.lo, sh.hi, epoch);
+                                                                   sh.lo, sh.hi);
   else
     reduce_scatter_kernel<__nv_bfloat16><<<grid, kCommThreads, 0, stream>>>(
-        P, rank, world, slot_base, sh.lo, sh.hi, epoch);
+        P, rank, world, slot_base, sh.lo, sh.hi);
   count_launch();
   return cudaGetLastError();
 }
@@ -207,13 +233,14 @@ cudaError_t launch_reduce_scatter_sm(const PeerPtrs& P, int rank, int world, int
 // ============================================================================
 // Barrier-only kernel (CE channel: the copy engines cannot wait on a flag).
 // ============================================================================
-__global__ void barrier_kernel(PeerPtrs P, int rank, int world, int set, uint32_t epoch) {
+__global__ void barrier_kernel(PeerPtrs P, int rank, int world, int set) {
+  const uint32_t epoch = take_epochs(P, rank, set, 1u) + 1u;
   peer_block_barrier(P, rank, world, set, 0, epoch);
 }
 
-cudaError_t launch_barrier(const PeerPtrs& P, int rank, int world, int set, uint32_t epoch,
+cudaError_t launch_barrier(const PeerPtrs& P, int rank, int world, int set,
                            cudaStream_t stream) {
-  barrier_kernel<<<1, 32, 0, stream>>>(P, rank, world, set, epoch);
+  barrier_kernel<<<1, 32, 0, stream>>>(P, rank, world, set);
   count_launch();
   return cudaGetLastError();
 }
@@ -261,10 +288,11 @@ cudaError_t launch_ce_reduce(char* own_grad_slot, const char* staging, int dtype
 template <typename T>
 __global__ void __launch_bounds__(kCommThreads) update_allgather_kernel(
     PeerPtrs P, int rank, int world, int64_t slot_base, int64_t lo, int64_t hi, float lr,
-    float momentum, float scale, float* __restrict__ mom, uint32_t epoch) {
+    float momentum, float scale, float* __restrict__ mom) {
   using V = Vec<T>;
   // entry: every rank's no-read window for this bucket is open
-  if (world > 1) peer_block_barrier(P, rank, world, kBarrierUpdate, blockIdx.x, 2u * epoch + 1u);
+  const uint32_t epoch = world > 1 ? take_epochs(P, rank, kBarrierUpdate, 2u) : 0u;
+  if (world > 1) peer_block_barrier(P, rank, world, kBarrierUpdate, blockIdx.x, epoch + 1u);
   const T* g = reinterpret_cast<const T*>(P.grads[rank]) + slot_base;
   float* own = P.params[rank];
 
@@ -310,21 +338,21 @@ __global__ void __launch_bounds__(kCommThreads) update_allgather_kernel(
       if (k < world) *reinterpret_cast<float4*>(P.params[k] + e) = q4;
   }
   // exit: every rank's stores into every parameter buffer have landed
-  if (world > 1) peer_block_barrier(P, rank, world, kBarrierUpdate, blockIdx.x, 2u * epoch + 2u);
+  if (world > 1) peer_block_barrier(P, rank, world, kBarrierUpdate, blockIdx.x, epoch + 2u);
 }
 
 cudaError_t launch_update_allgather(const PeerPtrs& P, int rank, int world, int dtype,
                                     int64_t slot_base, int64_t offset, int64_t numel, float lr,
                                     float momentum, float grad_scale, float* mom,
-                                    uint32_t epoch, cudaStream_t stream) {
+                                    cudaStream_t stream) {
   const ShardRange sh = shard_of(offset, numel, rank, world, dtype == 0 ? 4 : 8);
   const int grid = comm_grid_for((numel + world - 1) / world);
   if (dtype == 0)
     update_allgather_kernel<float><<<grid, kCommThreads, 0, stream>>>(
-        P, rank, world, slot_base, sh.lo, sh.hi, lr, momentum, grad_scale, mom, epoch);
+        P, rank, world, slot_base, sh.lo, sh.hi, lr, momentum, grad_scale, mom);
   else
     update_allgather_kernel<__nv_bfloat16><<<grid, kCommThreads, 0, stream>>>(
-        P, rank, world, slot_base, sh.lo, sh.hi, lr, momentum, grad_scale, mom, epoch);
+        P, rank, world, slot_base, sh.lo, sh.hi, lr, momentum, grad_scale, mom);
   count_launch();
   return cudaGetLastError();
 }

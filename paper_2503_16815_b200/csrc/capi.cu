@@ -317,14 +317,13 @@ struct deft_comm {
   int rank = 0, world = 1, dtype = 0, n_slots = 0;
   int64_t slot_elems = 0;
   PeerPtrs P{};
-  uint32_t epoch_rs = 0, epoch_ce = 0, epoch_up = 0;
   char* staging = nullptr;  // CE channel: (W-1) peer shards
   size_t staging_bytes = 0;
 };
 
 extern "C" size_t deft_comm_flag_bytes(int32_t world) {
   (void)world;
-  return (size_t)kNumBarrierSets * kMaxCommBlocks * kMaxWorld * sizeof(uint32_t);
+  return (size_t)kNumBarrierSets * kMaxCommBlocks * (kMaxWorld + 1) * sizeof(uint32_t);
 }
 
 extern "C" deft_status_t deft_comm_create(int32_t rank, int32_t world, void* const* grads,
@@ -379,7 +378,7 @@ extern "C" deft_status_t deft_bucket_reduce_scatter(deft_comm* c, int32_t channe
   const int64_t slot_base = (int64_t)slot * c->slot_elems;
   if (channel == DEFT_CHANNEL_SM) {
     cudaError_t e = launch_reduce_scatter_sm(c->P, c->rank, c->world, c->dtype, slot_base, offset,
-                                             numel, ++c->epoch_rs, s);
+                                             numel, s);
     if (e != cudaSuccess) return cuda_fail(e, "reduce_scatter_kernel");
     return DEFT_OK;
   }
@@ -398,7 +397,7 @@ extern "C" deft_status_t deft_bucket_reduce_scatter(deft_comm* c, int32_t channe
     DEFT_CUDA(cudaMalloc(&c->staging, need));
     c->staging_bytes = need;
   }
-  cudaError_t e = launch_barrier(c->P, c->rank, c->world, kBarrierCE, ++c->epoch_ce, s);
+  cudaError_t e = launch_barrier(c->P, c->rank, c->world, kBarrierCE, s);
   if (e != cudaSuccess) return cuda_fail(e, "barrier_kernel");
   if (len > 0) {
     int k = 0;
@@ -436,8 +435,7 @@ extern "C" deft_status_t deft_bucket_update(deft_comm* c, int32_t slot, int64_t 
     return DEFT_OK;
   }
   cudaError_t e = launch_update_allgather(c->P, c->rank, c->world, c->dtype, slot_base, offset,
-                                          numel, lr, momentum, grad_scale, d_mom, ++c->epoch_up,
-                                          s);
+                                          numel, lr, momentum, grad_scale, d_mom, s);
   if (e != cudaSuccess) return cuda_fail(e, "update_allgather_kernel");
   return DEFT_OK;
 }

@@ -35,7 +35,8 @@ int64_t smem_words_limit();
 // ---- bucket communication + fused update ----------------------------------
 constexpr int kMaxWorld = 8;
 constexpr int kMaxCommBlocks = 256;
-// flag area layout (uint32): [kNumBarrierSets][kMaxCommBlocks][kMaxWorld]
+// flag area layout (uint32): [kNumBarrierSets][kMaxCommBlocks][kMaxWorld] peer-written
+// epoch words, then [kNumBarrierSets][kMaxCommBlocks] rank-private epoch counters
 enum BarrierSet : int { kBarrierRS = 0, kBarrierCE = 1, kBarrierUpdate = 2, kNumBarrierSets = 3 };
 
 struct PeerPtrs {
@@ -67,8 +68,8 @@ int comm_grid_for(int64_t elems_per_rank);
 
 cudaError_t launch_reduce_scatter_sm(const PeerPtrs& P, int rank, int world, int dtype,
                                      int64_t slot_base, int64_t offset, int64_t numel,
-                                     uint32_t epoch, cudaStream_t stream);
-cudaError_t launch_barrier(const PeerPtrs& P, int rank, int world, int set, uint32_t epoch,
+                                     cudaStream_t stream);
+cudaError_t launch_barrier(const PeerPtrs& P, int rank, int world, int set,
                            cudaStream_t stream);
 cudaError_t launch_ce_reduce(char* own_grad_slot, const char* staging, int dtype, int world,
                              int rank, int64_t shard_lo, int64_t shard_len,
@@ -76,7 +77,7 @@ cudaError_t launch_ce_reduce(char* own_grad_slot, const char* staging, int dtype
 cudaError_t launch_update_allgather(const PeerPtrs& P, int rank, int world, int dtype,
                                     int64_t slot_base, int64_t offset, int64_t numel, float lr,
                                     float momentum, float grad_scale, float* mom,
-                                    uint32_t epoch, cudaStream_t stream);
+                                    cudaStream_t stream);
 cudaError_t launch_sgd_local(const void* grad, int dtype, float* param, float* mom,
                              int32_t count, const int64_t* offsets, const int64_t* numels,
                              const float* scales, float lr, float momentum,

@@ -1,0 +1,108 @@
+"""Bucket communication microbenchmark (BASELINE configs[4]: 1-256 MB buckets at
+2/4/8 GPUs vs the NCCL baseline).
+
+torchrun --nproc-per-node N tools/comm_bench.py [--sizes-mb 1,4,16,64,256]
+
+For each bucket size, timed with CUDA events on the launching stream after a
+barrier, max over ranks:
+  rs_sm     reduce-scatter, SM P2P channel        (deft_bucket_reduce_scatter ch 0)
+  rs_ce     reduce-scatter, copy-engine channel   (ch 1)
+  upd_ag    fused SGD/momentum + parameter all-gather (deft_bucket_update)
+  deft      rs_sm + upd_ag back to back = a full DeFT bucket sync incl. the update
+  nccl_ar   NCCL all_reduce (fp32 sum) of the bucket
+  nccl_ar_sgd  NCCL all_reduce + torch SGD/momentum on the bucket (the DDP baseline)
+Bus bandwidth: RS and AG move (W-1)/W of the bucket per rank each; AR 2(W-1)/W.
+"""
+import argparse
+import json
+import os
+import sys
+from pathlib import Path
+
+import torch
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from paper_2503_16815_b200 import _native  # noqa: E402
+from paper_2503_16815_b200.comm import BucketComm  # noqa: E402
+
+
+def timeit(fn, reps, warm, stream, device):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / reps], device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes-mb", default="1,4,16,64,256")
+    ap.add_argument("--reps", type=int, default=20)
+    args = ap.parse_args()
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    W, rank = dist.get_world_size(), dist.get_rank()
+    sizes = [int(x) for x in args.sizes_mb.split(",")]
+    max_elems = max(sizes) * 2**20 // 4
+    comm = BucketComm(rank, W, 1, max_elems, torch.float32, dev)
+    comm.grads.normal_()
+    mom = torch.zeros(max_elems, device=dev)
+    s = torch.cuda.Stream(dev)
+    rows = []
+    for mb in sizes:
+        n = mb * 2**20 // 4
+        nbytes = n * 4
+        res = {"bucket_mb": mb, "world": W}
+        with torch.cuda.stream(s):
+            res["rs_sm_ms"] = timeit(lambda: comm.reduce_scatter(_native.CHANNEL_SM, 0, 0, n, s),
+                                     args.reps, 3, s, dev)
+            res["rs_ce_ms"] = timeit(lambda: comm.reduce_scatter(_native.CHANNEL_CE, 0, 0, n, s),
+                                     args.reps, 3, s, dev)
+            res["upd_ag_ms"] = timeit(lambda: comm.update(0, 0, n, 1e-9, 0.9, 1e-3, mom, s),
+                                      args.reps, 3, s, dev)
+
+            def deft():
+                comm.reduce_scatter(_native.CHANNEL_SM, 0, 0, n, s)
+                comm.update(0, 0, n, 1e-9, 0.9, 1e-3, mom, s)
+            res["deft_ms"] = timeit(deft, args.reps, 3, s, dev)
+            x = torch.randn(n, device=dev)
+            p = torch.randn(n, device=dev)
+            v = torch.zeros(n, device=dev)
+            res["nccl_ar_ms"] = timeit(lambda: dist.all_reduce(x), args.reps, 3, s, dev)
+
+            def nccl_sgd():
+                dist.all_reduce(x)
+                v.mul_(0.9).add_(x, alpha=1e-3)
+                p.add_(v, alpha=-1e-9)
+            res["nccl_ar_sgd_ms"] = timeit(nccl_sgd, args.reps, 3, s, dev)
+        frac = (W - 1) / W
+        res["rs_sm_busbw_gbs"] = round(frac * nbytes / res["rs_sm_ms"] / 1e6, 1)
+        res["rs_ce_busbw_gbs"] = round(frac * nbytes / res["rs_ce_ms"] / 1e6, 1)
+        res["upd_ag_busbw_gbs"] = round(frac * nbytes / res["upd_ag_ms"] / 1e6, 1)
+        res["deft_busbw_gbs"] = round(2 * frac * nbytes / res["deft_ms"] / 1e6, 1)
+        res["nccl_ar_busbw_gbs"] = round(2 * frac * nbytes / res["nccl_ar_ms"] / 1e6, 1)
+        res["deft_vs_nccl_ar_sgd"] = round(res["nccl_ar_sgd_ms"] / res["deft_ms"], 3)
+        for k in list(res):
+            if k.endswith("_ms"):
+                res[k] = round(res[k], 4)
+        rows.append(res)
+        if rank == 0:
+            print(json.dumps(res), flush=True)
+    comm.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
