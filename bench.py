@@ -271,10 +271,12 @@ def main():
 
     for _ in range(args.warmup):
         ddp.train_step(batch, loss_fn)
-    n0 = _native.launch_count()
+    if ddp.static_batch is not None:
+        batch = ddp.static_batch      # graphs read these; no per-step device copy
+    n0 = ddp.native_launches()
     with ClockSampler(local) as clk:
         ms = timed(lambda: ddp.train_step(batch, loss_fn), args.steps)
-    launches = _native.launch_count() - n0
+    launches = ddp.native_launches() - n0
     ms_step = ms / args.steps
     value = args.batch * world * args.steps / (ms / 1e3)
 
@@ -282,7 +284,8 @@ def main():
     hx = batch[0].cpu().pin_memory()
     hy = batch[1].cpu().pin_memory()
     loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
-    dx, dy = torch.empty_like(batch[0]), torch.empty_like(batch[1])
+    dx, dy = batch if ddp.static_batch is not None else (torch.empty_like(batch[0]),
+                                                         torch.empty_like(batch[1]))
 
     def e2e_step():
         dx.copy_(hx, non_blocking=True)

@@ -24,20 +24,33 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
 namespace deft {
 
 constexpr int kCommThreads = 512;
-constexpr int kCommMaxBlocks = 32;      // leave the rest of the SMs to compute
 constexpr int kLocalThreads = 256;
 
+// CTAs per comm kernel: enough bytes in flight for NVLink, few enough to leave
+// the SMs to the concurrent forward/backward.  DEFT_COMM_BLOCKS overrides.
+static int comm_max_blocks() {
+  static int v = [] {
+    const char* e = getenv("DEFT_COMM_BLOCKS");
+    int x = e ? atoi(e) : 64;
+    if (x < 1) x = 1;
+    if (x > kMaxCommBlocks) x = kMaxCommBlocks;
+    return x;
+  }();
+  return v;
+}
+
 int comm_grid_for(int64_t elems_per_rank) {
-  const int64_t per_block = (int64_t)kCommThreads * 8 * 2;
+  const int64_t per_block = (int64_t)kCommThreads * 4 * 4;
   int64_t g = (elems_per_rank + per_block - 1) / per_block;
   if (g < 1) g = 1;
-  if (g > kCommMaxBlocks) g = kCommMaxBlocks;
+  if (g > comm_max_blocks()) g = comm_max_blocks();
   return (int)g;
 }
 
@@ -154,64 +167,82 @@ __device__ __forceinline__ Span split_span(int64_t lo, int64_t hi) {
 
 // ============================================================================
 // Reduce-scatter, SM channel: shard r = sum over ranks, written in place.
+// W is a template parameter so the peer pointers live in registers and every
+// loop unrolls; U = 16/W vectors per thread keep 16 independent 128-bit loads
+// in flight (the peer-load latency is ~2 us on NVLink).
 // ============================================================================
-template <typename T>
+template <typename T, int W>
 __global__ void __launch_bounds__(kCommThreads) reduce_scatter_kernel(
-    PeerPtrs P, int rank, int world, int64_t slot_base, int64_t lo, int64_t hi) {
+    PeerPtrs P, int rank, int64_t slot_base, int64_t lo, int64_t hi) {
   using V = Vec<T>;
+  using Raw = typename V::Raw;
+  constexpr int U = 16 / W > 0 ? 16 / W : 1;
   const uint32_t epoch = take_epochs(P, rank, kBarrierRS, 1u) + 1u;
-  peer_block_barrier(P, rank, world, kBarrierRS, blockIdx.x, epoch);
-  const T* src[kMaxWorld];
+  peer_block_barrier(P, rank, W, kBarrierRS, blockIdx.x, epoch);
+  const T* src[W];
 #pragma unroll
-  for (int k = 0; k < kMaxWorld; ++k)
-    src[k] = k < world ? reinterpret_cast<const T*>(P.grads[k]) + slot_base : nullptr;
+  for (int k = 0; k < W; ++k) src[k] = reinterpret_cast<const T*>(P.grads[k]) + slot_base;
   T* dst = reinterpret_cast<T*>(P.grads[rank]) + slot_base;
 
   const Span s = split_span<V::N>(lo, hi);
-  // scalar head / tail: handled by block 0
-  if (blockIdx.x == 0) {
+  if (blockIdx.x == 0) {  // unaligned edges
     for (int64_t e = s.head_lo + threadIdx.x; e < s.head_hi; e += blockDim.x) {
       float acc = 0.f;
-      for (int k = 0; k < world; ++k) acc += V::scalar(src[k] + e);
+#pragma unroll
+      for (int k = 0; k < W; ++k) acc += V::scalar(src[k] + e);
       V::put(dst + e, acc);
     }
     for (int64_t e = s.tail_lo + threadIdx.x; e < s.tail_hi; e += blockDim.x) {
       float acc = 0.f;
-      for (int k = 0; k < world; ++k) acc += V::scalar(src[k] + e);
+#pragma unroll
+      for (int k = 0; k < W; ++k) acc += V::scalar(src[k] + e);
       V::put(dst + e, acc);
     }
   }
   const int64_t nv = (s.body_hi - s.body_lo) / V::N;
   const int64_t v0 = s.body_lo / V::N;
-  using Raw = typename V::Raw;
-  constexpr int U = 2;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride * U) {
-    Raw raw[U][kMaxWorld];
+    Raw raw[U][W];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t vi = i + u * stride;
+      if (vi < nv) {
 #pragma unroll
-      for (int k = 0; k < kMaxWorld; ++k)
-        if (k < world && vi < nv) raw[u][k] = ld_nc(reinterpret_cast<const Raw*>(src[k]) + v0 + vi);
+        for (int k = 0; k < W; ++k) raw[u][k] = ld_nc(reinterpret_cast<const Raw*>(src[k]) + v0 + vi);
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t vi = i + u * stride;
-      if (vi >= nv) break;
-      float acc[V::N], tmp[V::N];
-      V::to_f32(raw[u][0], acc);
+      if (vi < nv) {
+        float acc[V::N], tmp[V::N];
+        V::to_f32(raw[u][0], acc);
 #pragma unroll
-      for (int k = 1; k < kMaxWorld; ++k) {
-        if (k < world) {
+        for (int k = 1; k < W; ++k) {
           V::to_f32(raw[u][k], tmp);
 #pragma unroll
           for (int c = 0; c < V::N; ++c) acc[c] += tmp[c];
         }
+        reinterpret_cast<Raw*>(dst)[v0 + vi] = V::from_f32(acc);
       }
-      reinterpret_cast<Raw*>(dst)[v0 + vi] = V::from_f32(acc);
     }
   }
+}
+
+template <typename T>
+static void rs_dispatch(int world, int grid, cudaStream_t stream, const PeerPtrs& P, int rank,
+                        int64_t slot_base, int64_t lo, int64_t hi) {
+#define DEFT_RS_CASE(WW) \
+  case WW:               \
+    reduce_scatter_kernel<T, WW><<<grid, kCommThreads, 0, stream>>>(P, rank, slot_base, lo, hi); \
+    break;
+  switch (world) {
+    DEFT_RS_CASE(2) DEFT_RS_CASE(3) DEFT_RS_CASE(4) DEFT_RS_CASE(5)
+    DEFT_RS_CASE(6) DEFT_RS_CASE(7) DEFT_RS_CASE(8)
+    default: break;
+  }
+#undef DEFT_RS_CASE
 }
 
 cudaError_t launch_reduce_scatter_sm(const PeerPtrs& P, int rank, int world, int dtype,
@@ -221,11 +252,9 @@ cudaError_t launch_reduce_scatter_sm(const PeerPtrs& P, int rank, int world, int
   const ShardRange sh = shard_of(offset, numel, rank, world, align);
   const int grid = comm_grid_for((numel + world - 1) / world);
   if (dtype == 0)
-    reduce_scatter_kernel<float><<<grid, kCommThreads, 0, stream>>>(P, rank, world, slot_base,
-                                                                   sh.lo, sh.hi);
+    rs_dispatch<float>(world, grid, stream, P, rank, slot_base, sh.lo, sh.hi);
   else
-    reduce_scatter_kernel<__nv_bfloat16><<<grid, kCommThreads, 0, stream>>>(
-        P, rank, world, slot_base, sh.lo, sh.hi);
+    rs_dispatch<__nv_bfloat16>(world, grid, stream, P, rank, slot_base, sh.lo, sh.hi);
   count_launch();
   return cudaGetLastError();
 }
@@ -285,60 +314,97 @@ cudaError_t launch_ce_reduce(char* own_grad_slot, const char* staging, int dtype
 // ============================================================================
 // Fused delayed SGD/momentum update of the owned shard + parameter all-gather.
 // ============================================================================
-template <typename T>
+template <typename T, int W>
 __global__ void __launch_bounds__(kCommThreads) update_allgather_kernel(
-    PeerPtrs P, int rank, int world, int64_t slot_base, int64_t lo, int64_t hi, float lr,
-    float momentum, float scale, float* __restrict__ mom) {
+    PeerPtrs P, int rank, int64_t slot_base, int64_t lo, int64_t hi, float lr, float momentum,
+    float scale, float* __restrict__ mom) {
   using V = Vec<T>;
+  constexpr int U = 2;
   // entry: every rank's no-read window for this bucket is open
-  const uint32_t epoch = world > 1 ? take_epochs(P, rank, kBarrierUpdate, 2u) : 0u;
-  if (world > 1) peer_block_barrier(P, rank, world, kBarrierUpdate, blockIdx.x, epoch + 1u);
+  const uint32_t epoch = take_epochs(P, rank, kBarrierUpdate, 2u);
+  peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 1u);
   const T* g = reinterpret_cast<const T*>(P.grads[rank]) + slot_base;
   float* own = P.params[rank];
+  float* dst[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) dst[k] = P.params[k];
 
-  auto step = [&](int64_t e, float gv) {
-    const float v = fmaf(momentum, mom[e], gv * scale);
-    mom[e] = v;
-    const float p = fmaf(-lr, v, own[e]);
-    for (int k = 0; k < world; ++k) P.params[k][e] = p;
-  };
-  // scalar edges (parameters are fp32: 4-element alignment)
-  const Span s = split_span<4>(lo, hi);
+  const Span s = split_span<4>(lo, hi);  // parameters are fp32: 4-element alignment
   if (blockIdx.x == 0) {
-    for (int64_t e = s.head_lo + threadIdx.x; e < s.head_hi; e += blockDim.x) step(e, V::scalar(g + e));
-    for (int64_t e = s.tail_lo + threadIdx.x; e < s.tail_hi; e += blockDim.x) step(e, V::scalar(g + e));
+    auto step = [&](int64_t e) {
+      const float v = fmaf(momentum, mom[e], V::scalar(g + e) * scale);
+      mom[e] = v;
+      const float p = fmaf(-lr, v, own[e]);
+#pragma unroll
+      for (int k = 0; k < W; ++k) dst[k][e] = p;
+    };
+    for (int64_t e = s.head_lo + threadIdx.x; e < s.head_hi; e += blockDim.x) step(e);
+    for (int64_t e = s.tail_lo + threadIdx.x; e < s.tail_hi; e += blockDim.x) step(e);
   }
   const int64_t nv = (s.body_hi - s.body_lo) / 4;
   const int64_t v0 = s.body_lo / 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
-    const int64_t e = (v0 + i) * 4;
-    float gv[4];
-    if constexpr (sizeof(T) == 4) {
-      const float4 r = *reinterpret_cast<const float4*>(g + e);
-      gv[0] = r.x; gv[1] = r.y; gv[2] = r.z; gv[3] = r.w;
-    } else {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride * U) {
+    float gv[U][4];
+    float4 m4[U], p4[U];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) gv[c] = V::scalar(g + e + c);
+    for (int u = 0; u < U; ++u) {
+      const int64_t vi = i + u * stride;
+      if (vi < nv) {
+        const int64_t e = (v0 + vi) * 4;
+        if constexpr (sizeof(T) == 4) {
+          const float4 r = __ldg(reinterpret_cast<const float4*>(g + e));
+          gv[u][0] = r.x; gv[u][1] = r.y; gv[u][2] = r.z; gv[u][3] = r.w;
+        } else {
+          const uint2 r = __ldg(reinterpret_cast<const uint2*>(g + e));
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+          const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+          gv[u][0] = a.x; gv[u][1] = a.y; gv[u][2] = b.x; gv[u][3] = b.y;
+        }
+        m4[u] = *reinterpret_cast<const float4*>(mom + e);
+        p4[u] = *reinterpret_cast<const float4*>(own + e);
+      }
     }
-    const float4 m4 = *reinterpret_cast<const float4*>(mom + e);
-    const float4 p4 = *reinterpret_cast<const float4*>(own + e);
-    float4 v4, q4;
-    v4.x = fmaf(momentum, m4.x, gv[0] * scale);
-    v4.y = fmaf(momentum, m4.y, gv[1] * scale);
-    v4.z = fmaf(momentum, m4.z, gv[2] * scale);
-    v4.w = fmaf(momentum, m4.w, gv[3] * scale);
-    q4.x = fmaf(-lr, v4.x, p4.x);
-    q4.y = fmaf(-lr, v4.y, p4.y);
-    q4.z = fmaf(-lr, v4.z, p4.z);
-    q4.w = fmaf(-lr, v4.w, p4.w);
-    *reinterpret_cast<float4*>(mom + e) = v4;
 #pragma unroll
-    for (int k = 0; k < kMaxWorld; ++k)
-      if (k < world) *reinterpret_cast<float4*>(P.params[k] + e) = q4;
+    for (int u = 0; u < U; ++u) {
+      const int64_t vi = i + u * stride;
+      if (vi < nv) {
+        const int64_t e = (v0 + vi) * 4;
+        float4 v4, q4;
+        v4.x = fmaf(momentum, m4[u].x, gv[u][0] * scale);
+        v4.y = fmaf(momentum, m4[u].y, gv[u][1] * scale);
+        v4.z = fmaf(momentum, m4[u].z, gv[u][2] * scale);
+        v4.w = fmaf(momentum, m4[u].w, gv[u][3] * scale);
+        q4.x = fmaf(-lr, v4.x, p4[u].x);
+        q4.y = fmaf(-lr, v4.y, p4[u].y);
+        q4.z = fmaf(-lr, v4.z, p4[u].z);
+        q4.w = fmaf(-lr, v4.w, p4[u].w);
+        *reinterpret_cast<float4*>(mom + e) = v4;
+#pragma unroll
+        for (int k = 0; k < W; ++k) *reinterpret_cast<float4*>(dst[k] + e) = q4;
+      }
+    }
   }
   // exit: every rank's stores into every parameter buffer have landed
-  if (world > 1) peer_block_barrier(P, rank, world, kBarrierUpdate, blockIdx.x, epoch + 2u);
+  peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 2u);
+}
+
+template <typename T>
+static void upd_dispatch(int world, int grid, cudaStream_t stream, const PeerPtrs& P, int rank,
+                         int64_t slot_base, int64_t lo, int64_t hi, float lr, float momentum,
+                         float scale, float* mom) {
+#define DEFT_UP_CASE(WW)                                                               \
+  case WW:                                                                             \
+    update_allgather_kernel<T, WW><<<grid, kCommThreads, 0, stream>>>(P, rank, slot_base, lo, \
+                                                                      hi, lr, momentum, scale, \
+                                                                      mom);            \
+    break;
+  switch (world) {
+    DEFT_UP_CASE(2) DEFT_UP_CASE(3) DEFT_UP_CASE(4) DEFT_UP_CASE(5)
+    DEFT_UP_CASE(6) DEFT_UP_CASE(7) DEFT_UP_CASE(8)
+    default: break;
+  }
+#undef DEFT_UP_CASE
 }
 
 cudaError_t launch_update_allgather(const PeerPtrs& P, int rank, int world, int dtype,
@@ -348,11 +414,11 @@ cudaError_t launch_update_allgather(const PeerPtrs& P, int rank, int world, int 
   const ShardRange sh = shard_of(offset, numel, rank, world, dtype == 0 ? 4 : 8);
   const int grid = comm_grid_for((numel + world - 1) / world);
   if (dtype == 0)
-    update_allgather_kernel<float><<<grid, kCommThreads, 0, stream>>>(
-        P, rank, world, slot_base, sh.lo, sh.hi, lr, momentum, grad_scale, mom);
+    upd_dispatch<float>(world, grid, stream, P, rank, slot_base, sh.lo, sh.hi, lr, momentum,
+                        grad_scale, mom);
   else
-    update_allgather_kernel<__nv_bfloat16><<<grid, kCommThreads, 0, stream>>>(
-        P, rank, world, slot_base, sh.lo, sh.hi, lr, momentum, grad_scale, mom);
+    upd_dispatch<__nv_bfloat16>(world, grid, stream, P, rank, slot_base, sh.lo, sh.hi, lr,
+                                momentum, grad_scale, mom);
   count_launch();
   return cudaGetLastError();
 }

@@ -33,8 +33,6 @@ future group's slot), so merging k iterations is plain gradient accumulation
 """
 from __future__ import annotations
 
-import math
-from collections import defaultdict
 from dataclasses import dataclass, field
 from typing import Callable
 
@@ -46,6 +44,7 @@ from .errors import DeftError, InternalInvariantError
 from .partition import PartitionConfig, element_ranges, partition_buckets
 from .preserver import WalkParams, feedback_loop
 from .profiles import BucketProfile, ClusterSpec, LinkSpec, ModelProfile
+from .planner import ExecutionPlanner, IterPlan
 from .scheduler import DeftScheduler, ScheduleDecision
 
 
@@ -62,6 +61,8 @@ class DeftConfig:
     lookahead: int = 32                     # decisions generated ahead of execution
     use_ce_channel: bool = True             # second link = copy engines
     instrument: bool = False                # CUDA events around every native launch
+    cuda_graphs: bool = True                # capture + replay each distinct iteration shape
+    graph_warmup: int = 1                   # eager runs of a shape before it is captured
 
 
 class _Bucket:
@@ -311,39 +312,41 @@ class DeftDataParallel:
                 self._bucket_nparams[b] += 1
         self.scheduler = DeftScheduler(part, cluster, mult)
         self.capacity_multiplier = mult
-        self._decisions: dict[int, tuple[ScheduleDecision, ScheduleDecision]] = {}
-        self._next_sched = 0
-        self.decision_log: list[tuple[ScheduleDecision, ScheduleDecision]] = []
+        self.planner = ExecutionPlanner(self.scheduler, self.cfg.n_slots, self.cfg.lookahead)
         self.link_streams = [torch.cuda.Stream(self.device) for _ in cluster.links]
         # runtime state
-        self._slot_of: dict[int, int] = {}
-        self._slot_free = [None] * self.cfg.n_slots   # event: slot reusable
-        self._slot_busy = [False] * self.cfg.n_slots
+        self._slot_free = [None] * self.cfg.n_slots   # event: slot reusable (async mode)
         self._rs_done: dict[tuple[int, int], torch.cuda.Event] = {}
-        self._group_left: dict[int, int] = {}
-        self._due_updates: list[tuple[int, int]] = []   # (group uid, merge_count)
         self._version_ready: torch.cuda.Event | None = None
         self._in_step = False
+        # CUDA graphs: iterations run strictly one after another (side streams
+        # join the compute stream at the end of each iteration)
+        self._sequential = self.cfg.cuda_graphs
+        self._graphs: dict = {}
+        self._seen: dict = {}
+        self._static = None
+        self._pool = torch.cuda.graph_pool_handle() if self.cfg.cuda_graphs else None
+        self._captured_native = 0
+        self._replayed_native = 0
         self._hooks = [p.register_post_accumulate_grad_hook(self._on_grad)
                        for p in self.params]
         return part
 
     def decisions(self, t: int) -> tuple[ScheduleDecision, ScheduleDecision]:
-        while self._next_sched <= t + self.cfg.lookahead:
-            k = self._next_sched
-            self._decisions[k] = (self.scheduler.schedule_forward(k),
-                                  self.scheduler.schedule_backward(k))
-            self._next_sched += 1
-        if t in self._decisions:
-            return self._decisions[t]
-        return self.decision_log[t]
+        return self.planner.decisions(t)
+
+    @property
+    def decision_log(self):
+        return self.planner.decision_log
 
     # ---------------------------------------------------------------- runtime
 
     def _autocast(self):
         if self.cfg.autocast_dtype is None:
             return torch.autocast("cuda", enabled=False)
-        return torch.autocast("cuda", dtype=self.cfg.autocast_dtype)
+        # the weight-cast cache must not outlive a CUDA-graph capture
+        return torch.autocast("cuda", dtype=self.cfg.autocast_dtype,
+                              cache_enabled=not self.cfg.cuda_graphs)
 
     def _bind_grads(self, slot: int):
         if self._bound_slot == slot:
@@ -351,19 +354,6 @@ class DeftDataParallel:
         for p, g in zip(self.params, self._grad_views[slot]):
             p.grad = g
         self._bound_slot = slot
-
-    def _slot_for(self, uid: int) -> int:
-        s = self._slot_of.get(uid)
-        if s is not None:
-            return s
-        for cand in range(self.cfg.n_slots):
-            if not self._slot_busy[cand]:
-                self._slot_busy[cand] = True
-                self._slot_of[uid] = cand
-                self._group_left[uid] = len(self.buckets)
-                return cand
-        raise InternalInvariantError(
-            f"all {self.cfg.n_slots} gradient slots are held by live groups; raise n_slots")
 
     def _timed(self, kind: str, stream, fn, nbytes: int):
         if not self.cfg.instrument:
@@ -375,30 +365,31 @@ class DeftDataParallel:
         b.record(stream)
         self._events_t.append((kind, a, b, nbytes))
 
-    def _issue_rs(self, tr, release: torch.cuda.Event):
+    def _issue_rs(self, link: int, slot: int, bidx: int, release: torch.cuda.Event):
         if self.world == 1:
             return
-        b = self.buckets[tr.bucket_id - 1]
-        s = self.link_streams[tr.link]
+        b = self.buckets[bidx]
+        s = self.link_streams[link]
         s.wait_event(release)
-        slot = self._slot_of[tr.group]
+        self._touched[id(s)] = s
         esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
         nbytes = (b.hi - b.lo) * esz * (self.world - 1) // self.world * 2
         self._timed("reduce_scatter", s,
-                    lambda: self.comm.reduce_scatter(self.channel_of_link[tr.link], slot, b.lo,
+                    lambda: self.comm.reduce_scatter(self.channel_of_link[link], slot, b.lo,
                                                      b.hi - b.lo, s), nbytes)
-        ev = torch.cuda.Event()
-        ev.record(s)
-        self._rs_done[(tr.group, tr.bucket_id)] = ev
+        if not self._sequential:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            self._rs_done[(slot, bidx)] = ev
 
-    def _issue_update(self, uid: int, k: int, bidx: int, window_open: torch.cuda.Event):
+    def _issue_update(self, slot: int, k: int, bidx: int, window_open: torch.cuda.Event):
         b = self.buckets[bidx]
         s = self.update_stream
         s.wait_event(window_open)
-        rs = self._rs_done.pop((uid, b.id), None)
+        self._touched[id(s)] = s
+        rs = self._rs_done.pop((slot, bidx), None)
         if rs is not None:
             s.wait_event(rs)
-        slot = self._slot_of[uid]
         esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
         shard = (b.hi - b.lo + self.world - 1) // self.world
         nbytes = shard * (esz + 4 * 4) + shard * 4 * (self.world - 1)
@@ -406,14 +397,6 @@ class DeftDataParallel:
                     lambda: self.comm.update(slot, b.lo, b.hi - b.lo, self.cfg.lr,
                                              self.cfg.momentum, 1.0 / (self.world * k),
                                              self.mom, s), nbytes)
-        self._group_left[uid] -= 1
-        if self._group_left[uid] == 0:
-            ev = torch.cuda.Event()
-            ev.record(s)
-            slot = self._slot_of.pop(uid)
-            del self._group_left[uid]
-            self._slot_free[slot] = ev
-            self._slot_busy[slot] = False
 
     def _on_grad(self, p):
         if not self._in_step:
@@ -427,52 +410,36 @@ class DeftDataParallel:
     def _bucket_ready(self, bidx: int):
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))
-        for tr in self._fresh.pop(bidx + 1, ()):
-            self._issue_rs(tr, ev)
-        for uid, k in self._due_updates:
-            self._issue_update(uid, k, bidx, ev)
+        for link, slot in self._fresh_now.pop(bidx, ()):
+            self._issue_rs(link, slot, bidx, ev)
+        for slot, k in self._due_now:
+            self._issue_update(slot, k, bidx, ev)
         self._fired[bidx] = True
 
-    def train_step(self, batch, loss_fn: Callable) -> torch.Tensor:
-        """One DeFT iteration: forward (Case 1 transfers released), backward
-        (Case 2/3/4 transfers, fresh ones per bucket), delayed updates."""
-        if not hasattr(self, "scheduler"):
-            raise DeftError("call plan() before train_step()")
-        if not hasattr(self, "_param_index"):
-            self._param_index = {id(p): i for i, p in enumerate(self.params)}
-        t = self.iteration
-        dF, dB = self.decisions(t)
-        self.decision_log.append(self._decisions.pop(t))
+    def _run_iteration(self, it: IterPlan, batch, loss_fn: Callable) -> torch.Tensor:
+        """Issue one iteration's device work on the current stream (+ link and
+        update streams).  Runs eagerly or inside a CUDA-graph capture."""
         comp = torch.cuda.current_stream(self.device)
-        if self._version_ready is not None:
+        self._touched = {}      # side streams forked from `comp` in this iteration
+        if not self._sequential and self._version_ready is not None:
             comp.wait_event(self._version_ready)   # theta^(t) complete
         ev_fwd = torch.cuda.Event()
         ev_fwd.record(comp)
-        for tr in dF.exec.transfers:
-            self._issue_rs(tr, ev_fwd)
+        for link, slot, bidx in it.fwd:
+            self._issue_rs(link, slot, bidx, ev_fwd)
         with self._autocast():
             loss = loss_fn(self.module, batch)
-        # backward stage: where do this iteration's gradients go?
-        uid = dB.exec.grad_group
-        if uid is None:
-            raise InternalInvariantError("backward decision without a gradient group")
-        new = uid not in self._slot_of
-        slot = self._slot_for(uid)
-        if new:
-            if dB.exec.grad_merge:
-                raise InternalInvariantError("merge into a group that has no slot")
-            if self._slot_free[slot] is not None:
-                comp.wait_event(self._slot_free[slot])
-            self.comm.grads[slot].zero_()
-        self._bind_grads(slot)
+        if it.zero:
+            if not self._sequential and self._slot_free[it.slot] is not None:
+                comp.wait_event(self._slot_free[it.slot])
+            self.comm.grads[it.slot].zero_()
+        self._bind_grads(it.slot)
         ev_bwd = torch.cuda.Event()
         ev_bwd.record(comp)
-        self._fresh = defaultdict(list)
-        for tr in dB.exec.transfers:
-            if tr.fresh:
-                self._fresh[tr.bucket_id].append(tr)
-            else:
-                self._issue_rs(tr, ev_bwd)
+        for link, slot, bidx in it.bwd:
+            self._issue_rs(link, slot, bidx, ev_bwd)
+        self._fresh_now = dict(it.fresh)
+        self._due_now = it.due
         self._pending = list(self._bucket_nparams)
         self._fired = [False] * len(self.buckets)
         self._in_step = True
@@ -483,14 +450,72 @@ class DeftDataParallel:
         for b in range(len(self.buckets)):      # buckets whose params got no gradient
             if not self._fired[b]:
                 self._bucket_ready(b)
-        if self._fresh:
+        if self._fresh_now:
             raise InternalInvariantError("fresh transfers left unreleased")
-        ev = torch.cuda.Event()
-        ev.record(self.update_stream)
-        self._version_ready = ev
-        # events of THIS decision are applied during the next backward (visible at t+2)
-        self._due_updates = [(u, k) for u, k, _ in dB.exec.updates]
+        if self._sequential:
+            for s in self._touched.values():   # join (only streams forked this iteration)
+                comp.wait_stream(s)
+        else:
+            ev = torch.cuda.Event()
+            ev.record(self.update_stream)
+            self._version_ready = ev
+            for fs in it.freed:
+                self._slot_free[fs] = ev
+        return loss
+
+    def _static_inputs(self, batch):
+        if self._static is None:
+            self._static = tuple(x.detach().clone() for x in batch)
+        if any(a is not b for a, b in zip(self._static, batch)):
+            for dst, src in zip(self._static, batch):
+                dst.copy_(src, non_blocking=True)
+        return self._static
+
+    @property
+    def static_batch(self):
+        """The input tensors captured graphs read (CUDA-graph mode); writing the
+        next batch straight into them saves a device copy."""
+        return self._static
+
+    def native_launches(self) -> int:
+        """Native kernels launched (captured kernels count once per replay)."""
+        return _native.launch_count() - self._captured_native + self._replayed_native
+
+    def train_step(self, batch, loss_fn: Callable) -> torch.Tensor:
+        """One DeFT iteration: forward (Case 1 transfers released), backward
+        (Case 2/3/4 transfers, fresh ones per bucket), delayed updates.
+        With ``cuda_graphs`` the device work of every distinct iteration shape is
+        captured once (after one eager run) and replayed; the returned loss is
+        then a static tensor, valid until the next step."""
+        if not hasattr(self, "scheduler"):
+            raise DeftError("call plan() before train_step()")
+        if not hasattr(self, "_param_index"):
+            self._param_index = {id(p): i for i, p in enumerate(self.params)}
+        it = self.planner.plan(self.iteration)
         self.iteration += 1
+        if not self._sequential or self.cfg.instrument:
+            return self._run_iteration(it, batch, loss_fn)
+        static = self._static_inputs(batch)
+        hit = self._graphs.get(it.key)
+        if hit is not None:
+            g, loss, n = hit
+            g.replay()
+            self._replayed_native += n
+            return loss
+        seen = self._seen.get(it.key, 0)
+        self._seen[it.key] = seen + 1
+        if seen < self.cfg.graph_warmup:
+            return self._run_iteration(it, static, loss_fn)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        n0 = _native.launch_count()
+        with torch.cuda.graph(g, pool=self._pool):
+            loss = self._run_iteration(it, static, loss_fn)
+        n = _native.launch_count() - n0
+        self._captured_native += n
+        self._graphs[it.key] = (g, loss, n)
+        g.replay()
+        self._replayed_native += n
         return loss
 
     def finish(self):

@@ -1,0 +1,103 @@
+"""Host bookkeeping of the executor, free of any device work.
+
+Turns the decision stream of a ``DeftScheduler`` into per-iteration execution
+plans: which gradient slot every transfer reads, which slot this iteration's
+gradients accumulate into (store = fresh zeroed slot, merge = the live future
+group's slot), and which group updates run in this iteration's backward
+(update events of decision (t-1, backward); visible from t+1 = (t-1)+2).
+Kept separate from ``executor.py`` so the slot/group invariants can be
+checked on CPU over every golden decision stream (tests/test_planner.py).
+"""
+from __future__ import annotations
+
+from collections import defaultdict
+from dataclasses import dataclass
+
+from .errors import InternalInvariantError
+from .scheduler import DeftScheduler, ScheduleDecision
+
+
+@dataclass(frozen=True)
+class IterPlan:
+    t: int
+    slot: int                 # gradient slot this iteration accumulates into
+    zero: bool                # new group (store): zero the slot first
+    fwd: tuple                # (link, slot, bucket index) released at forward start
+    bwd: tuple                # ... released at backward start
+    fresh: tuple              # (bucket index, ((link, slot), ...)) released at bucket end
+    due: tuple                # (slot, merge_count) updates applied per bucket this backward
+    freed: tuple              # slots whose group is fully updated after this iteration
+    key: tuple                # identifies the device work (CUDA-graph cache key)
+
+
+class ExecutionPlanner:
+    def __init__(self, scheduler: DeftScheduler, n_slots: int, lookahead: int = 32):
+        self.scheduler = scheduler
+        self.n_slots = n_slots
+        self.lookahead = lookahead
+        self._decisions: dict[int, tuple[ScheduleDecision, ScheduleDecision]] = {}
+        self._next = 0
+        self.decision_log: list[tuple[ScheduleDecision, ScheduleDecision]] = []
+        self._slot_of: dict[int, int] = {}
+        self._busy = [False] * n_slots
+        self._due_groups: list[tuple[int, int]] = []
+
+    def decisions(self, t: int) -> tuple[ScheduleDecision, ScheduleDecision]:
+        while self._next <= t + self.lookahead:
+            k = self._next
+            self._decisions[k] = (self.scheduler.schedule_forward(k),
+                                  self.scheduler.schedule_backward(k))
+            self._next += 1
+        if t in self._decisions:
+            return self._decisions[t]
+        return self.decision_log[t]
+
+    def live_slots(self) -> dict[int, int]:
+        return dict(self._slot_of)
+
+    def _alloc(self, uid: int) -> int:
+        for cand in range(self.n_slots):
+            if not self._busy[cand]:
+                self._busy[cand] = True
+                self._slot_of[uid] = cand
+                return cand
+        raise InternalInvariantError(
+            f"all {self.n_slots} gradient slots are held by live groups; raise n_slots")
+
+    def plan(self, t: int) -> IterPlan:
+        if t != len(self.decision_log):
+            raise InternalInvariantError("iterations must be planned in order")
+        dF, dB = self.decisions(t)
+        self.decision_log.append(self._decisions.pop(t))
+        fwd = tuple((tr.link, self._slot_of[tr.group], tr.bucket_id - 1)
+                    for tr in dF.exec.transfers)
+        uid = dB.exec.grad_group
+        if uid is None:
+            raise InternalInvariantError("backward decision without a gradient group")
+        new = uid not in self._slot_of
+        if new and dB.exec.grad_merge:
+            raise InternalInvariantError("merge into a group that has no slot")
+        if not new and not dB.exec.grad_merge:
+            raise InternalInvariantError("store into a group that already has a slot")
+        bwd, fresh = [], defaultdict(list)
+        for tr in dB.exec.transfers:       # older groups first: their slots exist
+            if tr.group != uid:
+                bwd.append((tr.link, self._slot_of[tr.group], tr.bucket_id - 1))
+        slot = self._slot_of[uid] if not new else self._alloc(uid)
+        for tr in dB.exec.transfers:
+            if tr.group == uid:
+                if tr.fresh:
+                    fresh[tr.bucket_id - 1].append((tr.link, slot))
+                else:
+                    bwd.append((tr.link, slot, tr.bucket_id - 1))
+        # groups reported by decision (t-1, backward) are updated in this backward
+        due = tuple((self._slot_of[u], k) for u, k in self._due_groups)
+        freed = []
+        for u, _ in self._due_groups:
+            s = self._slot_of.pop(u)
+            self._busy[s] = False
+            freed.append(s)
+        self._due_groups = [(u, k) for u, k, _ in dB.exec.updates]
+        fresh_t = tuple(sorted((b, tuple(v)) for b, v in fresh.items()))
+        key = (fwd, slot, new, tuple(bwd), fresh_t, due)
+        return IterPlan(t, slot, new, fwd, tuple(bwd), fresh_t, due, tuple(freed), key)

@@ -65,11 +65,12 @@ def equal_dual():
 
 
 def run_executor(world, rank, iterations, n_buckets=48, total=48_000, lr=0.05, momentum=0.9,
-                 grad_dtype=torch.float32, comm_us=900, group=None):
+                 grad_dtype=torch.float32, comm_us=900, group=None, cuda_graphs=True):
     """Run the executor on the probe; return (theta^(T) flat CPU, decisions as dicts)."""
     model = Probe(probe_sizes(total)).cuda()
     cfg = D.DeftConfig(lr=lr, momentum=momentum, autocast_dtype=None, grad_dtype=grad_dtype,
-                       partition=D.PartitionConfig(partition_size=10**9))
+                       partition=D.PartitionConfig(partition_size=10**9),
+                       cuda_graphs=cuda_graphs)
     ddp = D.DeftDataParallel(model, cfg, process_group=group)
     prof = uniform_profile(n_buckets, total // n_buckets, comm_us=comm_us)
     ddp.plan(prof, equal_dual())

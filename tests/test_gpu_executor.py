@@ -17,9 +17,11 @@ def need_gpu():
         pytest.skip("no CUDA device")
 
 
+@pytest.mark.parametrize("graphs", [True, False])
 @pytest.mark.parametrize("iterations,comm_us", [(12, 900), (25, 900), (20, 300), (16, 1900)])
-def test_single_gpu_matches_oracle(iterations, comm_us):
-    theta, theta0, decisions = S.run_executor(1, 0, iterations, comm_us=comm_us)
+def test_single_gpu_matches_oracle(iterations, comm_us, graphs):
+    theta, theta0, decisions = S.run_executor(1, 0, iterations, comm_us=comm_us,
+                                              cuda_graphs=graphs)
     want = S.oracle_theta(theta0, decisions, 1, iterations)
     assert S.rel_err(theta, want) <= S.TOL
 
@@ -32,22 +34,24 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, iterations, comm_us, q):
+def _worker(rank, world, port, iterations, comm_us, graphs, q):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world,
                             device_id=torch.device("cuda", rank))
     try:
-        theta, theta0, decisions = S.run_executor(world, rank, iterations, comm_us=comm_us)
+        theta, theta0, decisions = S.run_executor(world, rank, iterations, comm_us=comm_us,
+                                                  cuda_graphs=graphs)
         q.put((rank, theta, theta0, decisions))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.multigpu
+@pytest.mark.parametrize("graphs", [True, False])
 @pytest.mark.parametrize("iterations,comm_us", [(14, 900), (20, 1900)])
-def test_multi_gpu_matches_oracle(iterations, comm_us):
+def test_multi_gpu_matches_oracle(iterations, comm_us, graphs):
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -55,7 +59,7 @@ def test_multi_gpu_matches_oracle(iterations, comm_us):
     ctx = torch.multiprocessing.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, iterations, comm_us, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, iterations, comm_us, graphs, q))
              for r in range(world)]
     for p in procs:
         p.start()

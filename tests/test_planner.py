@@ -1,0 +1,143 @@
+"""The executor's host bookkeeping (planner.py) over every golden decision
+stream: slot lifetimes, merges, transfer coverage, update timing -- on CPU,
+plus a world_size-2 gloo run showing every rank plans identical device work."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT  # noqa: F401
+from oracle import deft_oracle as O
+import paper_2503_16815_b200 as D
+from paper_2503_16815_b200 import knapsack as K
+from paper_2503_16815_b200.planner import ExecutionPlanner
+from test_host_logic import build_product_inputs
+
+
+def _planner_for(entry, inputs, n_slots=5):
+    prof, cluster, cfg, mult, iters = build_product_inputs(entry, inputs)
+    part = D.partition_buckets(prof, cfg) if cfg is not None else prof
+    return ExecutionPlanner(D.DeftScheduler(part, cluster, mult), n_slots), part, iters
+
+
+def check_invariants(planner, n_buckets, iters):
+    live = {}            # slot -> set of bucket indices still to transfer for its group
+    pending_update = {}  # slot -> merge_count, group fully sent, update next iteration
+    for t in range(iters):
+        p = planner.plan(t)
+        # updates due now: groups reported last iteration, all buckets sent
+        for slot, k in p.due:
+            assert slot in pending_update and pending_update.pop(slot) == k
+        for link, slot, b in p.fwd + p.bwd:
+            assert slot in live and b in live[slot], (t, slot, b)
+            live[slot].discard(b)
+        if p.zero:
+            assert p.slot not in live and p.slot not in pending_update, "slot reused while live"
+            live[p.slot] = set(range(n_buckets))
+        else:
+            assert p.slot in live
+        for b, pairs in p.fresh:
+            for link, slot in pairs:
+                assert slot == p.slot and b in live[slot]
+                live[slot].discard(b)
+        d_b = planner.decision_log[t][1]
+        for uid, k, _ in d_b.exec.updates:
+            # the group's slot is fully sent when its event is reported
+            emptied = [s for s, left in live.items() if not left and s not in pending_update]
+            assert emptied, (t, uid)
+        for s in [s for s, left in live.items() if not left]:
+            pending_update[s] = None
+        for s in list(pending_update):
+            if pending_update[s] is None:
+                del live[s]
+        # attach merge counts to the groups reported in this decision
+        reported = [k for _, k, _ in d_b.exec.updates]
+        empty_slots = [s for s, v in pending_update.items() if v is None]
+        assert len(empty_slots) == len(reported), (t, empty_slots, reported)
+        for s, k in zip(sorted(empty_slots, key=lambda s: -1), reported):
+            pending_update[s] = k
+        assert len(live) + len(pending_update) <= planner.n_slots
+
+
+@pytest.fixture(autouse=True)
+def oracle_dp():
+    with K.subset_sum_backend(O.subset_sum_c_batch):
+        yield
+
+
+def test_planner_invariants_on_golden_streams(golden_index, golden_inputs):
+    checked = 0
+    for e in golden_index:
+        if len(e["partitioned"]) > 60:
+            continue
+        planner, part, iters = _planner_for(e, golden_inputs)
+        check_invariants(planner, part.n_buckets, min(iters, 120))
+        checked += 1
+    assert checked >= 45
+
+
+def test_steady_state_shapes_are_few(golden_inputs):
+    """CUDA-graph mode captures one graph per distinct iteration shape.  In the
+    NVLink regime (coverage rate << 1: every bucket fits its backward window)
+    the steady state needs at most two shapes (slot ping-pong)."""
+    for name in ("resnet101", "vgg19", "gpt2"):
+        prof = D.profile_from_dict(golden_inputs["profiles"][name]).scaled_comm(0.01)
+        cluster = D.cluster_from_dict(golden_inputs["clusters"]["dual"])
+        part = D.partition_buckets(prof, D.PartitionConfig(6_500_000, mu=1.65))
+        planner = ExecutionPlanner(D.DeftScheduler(part, cluster), 5)
+        keys = [planner.plan(t).key for t in range(40)]
+        assert len(set(keys[4:])) <= 2, name
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _gloo_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import json
+        from conftest import GOLDEN
+        inputs = json.loads((GOLDEN / "inputs.json").read_text())
+        index = json.loads((GOLDEN / "schedules.json").read_text())
+        entry = next(e for e in index if e["key"] == "vgg19__dual__bw0.25")
+        with K.subset_sum_backend(O.subset_sum_c_batch):
+            planner, part, iters = _planner_for(entry, inputs)
+            keys = [planner.plan(t).key for t in range(60)]
+        gathered = [None] * world
+        dist.all_gather_object(gathered, keys)
+        # and the delayed-SGD oracle's gloo reduction equals the local sum
+        from oracle import delayed_sgd
+        decisions = [d.to_dict() for pair in planner.decision_log for d in pair]
+        theta0 = torch.linspace(-1, 1, 64)
+        grad = lambda th, r, t: torch.sin(th * (t + 1) + r)  # noqa: E731
+        got = delayed_sgd.run(theta0, grad, decisions, world, 0.1, 0.9, 40, reduce="gloo",
+                              rank=rank)
+        want = delayed_sgd.run(theta0, grad, decisions, world, 0.1, 0.9, 40)
+        q.put((rank, all(g == keys for g in gathered), float((got - want).abs().max())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_plans_agree():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, same, err in res:
+        assert same, rank
+        assert err < 1e-6, (rank, err)
