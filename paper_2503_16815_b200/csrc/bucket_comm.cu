@@ -38,7 +38,7 @@ constexpr int kLocalThreads = 256;
 static int comm_max_blocks() {
   static int v = [] {
     const char* e = getenv("DEFT_COMM_BLOCKS");
-    int x = e ? atoi(e) : 64;
+    int x = e ? atoi(e) : 128;
     if (x < 1) x = 1;
     if (x > kMaxCommBlocks) x = kMaxCommBlocks;
     return x;
@@ -47,7 +47,7 @@ static int comm_max_blocks() {
 }
 
 int comm_grid_for(int64_t elems_per_rank) {
-  const int64_t per_block = (int64_t)kCommThreads * 4 * 4;
+  const int64_t per_block = 16384;  // ~64 KB of fp32 per rank per CTA
   int64_t g = (elems_per_rank + per_block - 1) / per_block;
   if (g < 1) g = 1;
   if (g > comm_max_blocks()) g = comm_max_blocks();

@@ -94,7 +94,7 @@ class DeftDataParallel:
                                self.cfg.grad_dtype, self.device, process_group)
         self.mom = torch.zeros(self.total, dtype=torch.float32, device=self.device)
         self._bind_params()
-        self.compute = torch.cuda.current_stream(self.device)
+        self.compute_stream = torch.cuda.Stream(self.device)
         prio_lo, prio_hi = torch.cuda.Stream.priority_range()
         self.update_stream = torch.cuda.Stream(self.device, priority=prio_hi)
         self.link_streams: list[torch.cuda.Stream] = []
@@ -452,6 +452,7 @@ class DeftDataParallel:
                 self._bucket_ready(b)
         if self._fresh_now:
             raise InternalInvariantError("fresh transfers left unreleased")
+        loss = loss.detach()  # drop the autograd graph (no stale AccumulateGrad nodes)
         if self._sequential:
             for s in self._touched.values():   # join (only streams forked this iteration)
                 comp.wait_stream(s)
@@ -484,15 +485,25 @@ class DeftDataParallel:
     def train_step(self, batch, loss_fn: Callable) -> torch.Tensor:
         """One DeFT iteration: forward (Case 1 transfers released), backward
         (Case 2/3/4 transfers, fresh ones per bucket), delayed updates.
-        With ``cuda_graphs`` the device work of every distinct iteration shape is
-        captured once (after one eager run) and replayed; the returned loss is
-        then a static tensor, valid until the next step."""
+        Returns the (detached) loss.  With ``cuda_graphs`` the device work of
+        every distinct iteration shape is captured once (after one eager run)
+        and replayed; the loss is then a static tensor, valid until the next step.
+        All device work runs on the executor's own compute stream, ordered after
+        the caller's current stream and before its next work."""
         if not hasattr(self, "scheduler"):
             raise DeftError("call plan() before train_step()")
         if not hasattr(self, "_param_index"):
             self._param_index = {id(p): i for i, p in enumerate(self.params)}
         it = self.planner.plan(self.iteration)
         self.iteration += 1
+        caller = torch.cuda.current_stream(self.device)
+        self.compute_stream.wait_stream(caller)
+        with torch.cuda.stream(self.compute_stream):
+            loss = self._dispatch(it, batch, loss_fn)
+        caller.wait_stream(self.compute_stream)
+        return loss
+
+    def _dispatch(self, it: IterPlan, batch, loss_fn: Callable) -> torch.Tensor:
         if not self._sequential or self.cfg.instrument:
             return self._run_iteration(it, batch, loss_fn)
         static = self._static_inputs(batch)
@@ -506,10 +517,10 @@ class DeftDataParallel:
         self._seen[it.key] = seen + 1
         if seen < self.cfg.graph_warmup:
             return self._run_iteration(it, static, loss_fn)
-        torch.cuda.synchronize(self.device)
+        self.compute_stream.synchronize()
         g = torch.cuda.CUDAGraph()
         n0 = _native.launch_count()
-        with torch.cuda.graph(g, pool=self._pool):
+        with torch.cuda.graph(g, pool=self._pool, stream=self.compute_stream):
             loss = self._run_iteration(it, static, loss_fn)
         n = _native.launch_count() - n0
         self._captured_native += n
