@@ -37,7 +37,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--model", default="resnet101", choices=["resnet101", "vgg19", "gpt2"])
     ap.add_argument("--impl", default="deft", choices=["deft", "reference"])
-    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--batch", type=int, default=None,
+                    help="per-GPU batch (default 64; GPT-2: 16 sequences of 1024)")
+    ap.add_argument("--update-placement", default="bucket", choices=["bucket", "end"])
+    ap.add_argument("--eager", action="store_true", help="no CUDA graphs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -63,7 +66,10 @@ def build_model(name, device):
     else:
         from transformers import GPT2Config, GPT2LMHeadModel
         m = GPT2LMHeadModel(GPT2Config(n_positions=1024))
+        m.config.use_cache = False
     m = m.to(device)
+    if name == "gpt2" and device != "cpu":
+        m = m.to(torch.bfloat16)  # BASELINE configs[3]: bf16 gradient buckets
     if name != "gpt2":
         m = m.to(memory_format=torch.channels_last)
     return m
@@ -208,7 +214,8 @@ def compute_only_step_ms(model, batch, loss_fn, steps, warmup, world, dist, devi
 
     def step():
         opt.zero_grad(set_to_none=False)
-        with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
+        with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False,
+                            enabled=next(model.parameters()).dtype == torch.float32):
             loss = loss_fn(model, batch)
         loss.backward()
         opt.step()
@@ -280,8 +287,12 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
 
     saved_p = ddp.comm.params.clone()
     saved_m = ddp.mom.clone()
-    upd_bytes = sum(((b.hi - b.lo + world - 1) // world) * (esz + 16 + 4 * (world - 1))
-                    for b in ddp.buckets)
+    if ddp.cfg.grad_dtype == torch.bfloat16:   # g 2 + v 8 + master 8 + bf16 p to W ranks
+        esz = 2
+        per = lambda w: 2 + 16 + 2 * w  # noqa: E731
+    else:                                     # g 4 + v 8 + p 8 (+4 per extra rank)
+        per = lambda w: 4 + 16 + 4 * (w - 1)  # noqa: E731
+    upd_bytes = sum(((b.hi - b.lo + world - 1) // world) * per(world) for b in ddp.buckets)
 
     def updates():
         for b in ddp.buckets:
@@ -304,6 +315,8 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
 
 def main():
     args = parse()
+    if args.batch is None:
+        args.batch = 16 if args.model == "gpt2" else BATCH
     import torch
     import torch.distributed as dist
 
@@ -345,7 +358,9 @@ def main():
     # 2) DeFT: profile on this GPU, plan (partition + feedback loop), run
     walk = D.WalkParams.from_dict(
         json.loads((ROOT / "tests" / "golden" / "inputs.json").read_text())["walk"])
-    cfg = D.DeftConfig(lr=0.1, momentum=0.9, walk=walk,
+    cfg = D.DeftConfig(lr=0.1, momentum=0.9, walk=walk, cuda_graphs=not args.eager,
+                       update_placement=args.update_placement,
+                       autocast_dtype=None if args.model == "gpt2" else torch.bfloat16,
                        partition=D.PartitionConfig(partition_size=6_500_000, mu=1.0))
     ddp = D.DeftDataParallel(model, cfg)
     t_setup = time.perf_counter()
@@ -454,7 +469,9 @@ def main():
                                                            else ", seq 1024"),
                        "model": args.model, "global_batch": args.batch * world,
                        "parallelism": f"dp{world}", "l2": "working set (activations) >> L2 126 MB",
-                       "grad_dtype": "fp32", "compute": "bf16 autocast",
+                       "grad_dtype": str(ddp.cfg.grad_dtype).replace("torch.", ""),
+                       "compute": "bf16 autocast" if args.model != "gpt2" else "bf16 weights",
+                       "update_placement": ddp.cfg.update_placement,
                        "buckets": part.n_buckets, "links": [l.name for l in ddp.cluster.links],
                        "capacity_multiplier": ddp.capacity_multiplier,
                        "cuda_graphs": ddp.cfg.cuda_graphs, "setup_s": round(t_setup, 2)},

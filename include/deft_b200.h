@@ -97,16 +97,20 @@ deft_status_t deft_mem_close(void* d_peer_ptr);
  * Communicator: one per rank over W <= 8 ranks of one NVSwitch node.
  *   grads[r]  : rank r's gradient arena (n_slots group buffers of `slot_elems`
  *               elements each) -- what autograd writes, what peers read;
- *   params[r] : rank r's flat parameter buffer (fp32, output-side bucket first);
- *   flags[r]  : rank r's barrier flag area (deft_comm_flag_bytes()).
+ *   params[r] : rank r's flat parameter buffer, output-side bucket first, in the
+ *               gradient dtype (fp32, or bf16 for bf16-gradient models);
+ *   flags[r]  : rank r's barrier flag area (deft_comm_flag_bytes());
+ *   d_master  : this rank's fp32 master parameters (required for bf16, else NULL):
+ *               the update reads/writes it and stores bf16 copies to params[*].
  * Pointer arrays are HOST arrays of already-mapped device pointers (own
  * pointer at index `rank`).
  * ------------------------------------------------------------------------ */
 typedef struct deft_comm deft_comm;
 size_t deft_comm_flag_bytes(int32_t world);
 deft_status_t deft_comm_create(int32_t rank, int32_t world, void* const* grads,
-                               void* const* params, void* const* flags, int64_t slot_elems,
-                               int32_t n_slots, int32_t grad_dtype, deft_comm** out);
+                               void* const* params, void* const* flags, float* d_master,
+                               int64_t slot_elems, int32_t n_slots, int32_t grad_dtype,
+                               deft_comm** out);
 deft_status_t deft_comm_destroy(deft_comm* c);
 
 /* grad_dtype codes */
@@ -137,15 +141,17 @@ deft_status_t deft_bucket_update(deft_comm* c, int32_t slot, int64_t offset, int
                                  void* stream);
 
 /* Local (W == 1 or rank-private) fused update over device arrays:
- * v = m*v + s*g ; p -= lr*v. grad_dtype as above. */
-deft_status_t deft_sgd_momentum_update(const void* d_grad, int32_t grad_dtype, float* d_param,
-                                       float* d_mom, int64_t numel, float lr, float momentum,
-                                       float grad_scale, void* stream);
+ * v = m*v + s*g ; p -= lr*v. grad_dtype as above; d_param has the grad dtype;
+ * for bf16 the fp32 master d_master is updated and rounded into d_param. */
+deft_status_t deft_sgd_momentum_update(const void* d_grad, int32_t grad_dtype, void* d_param,
+                                       float* d_master, float* d_mom, int64_t numel, float lr,
+                                       float momentum, float grad_scale, void* stream);
 
 /* Multi-bucket variant: one launch updates `count` (offset, numel, scale)
  * segments of the same arrays (the buckets of one update event). Host arrays. */
 deft_status_t deft_sgd_momentum_update_multi(const void* d_grad, int32_t grad_dtype,
-                                             float* d_param, float* d_mom, int32_t count,
+                                             void* d_param, float* d_master, float* d_mom,
+                                             int32_t count,
                                              const int64_t* offsets, const int64_t* numels,
                                              const float* grad_scales, float lr,
                                              float momentum, void* stream);

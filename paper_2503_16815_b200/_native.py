@@ -59,16 +59,17 @@ def _declare(lib):
         "deft_mem_open": (c_i32, [P(ctypes.c_uint8), P(c_vp)]),
         "deft_mem_close": (c_i32, [c_vp]),
         "deft_comm_flag_bytes": (c_sz, [c_i32]),
-        "deft_comm_create": (c_i32, [c_i32, c_i32, P(c_vp), P(c_vp), P(c_vp), c_i64, c_i32,
-                                     c_i32, P(c_vp)]),
+        "deft_comm_create": (c_i32, [c_i32, c_i32, P(c_vp), P(c_vp), P(c_vp), c_vp, c_i64,
+                                     c_i32, c_i32, P(c_vp)]),
         "deft_comm_destroy": (c_i32, [c_vp]),
         "deft_bucket_reduce_scatter": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i64, c_vp]),
         "deft_bucket_update": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_f32, c_f32, c_f32, c_vp,
                                        c_vp]),
-        "deft_sgd_momentum_update": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i64, c_f32, c_f32,
-                                             c_f32, c_vp]),
-        "deft_sgd_momentum_update_multi": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, P(c_i64),
-                                                   P(c_i64), P(c_f32), c_f32, c_f32, c_vp]),
+        "deft_sgd_momentum_update": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_i64, c_f32,
+                                             c_f32, c_f32, c_vp]),
+        "deft_sgd_momentum_update_multi": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_i32,
+                                                   P(c_i64), P(c_i64), P(c_f32), c_f32, c_f32,
+                                                   c_vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

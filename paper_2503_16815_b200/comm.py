@@ -71,7 +71,11 @@ class BucketComm:
         ipc = world > 1
         self.grads, self._g = region_tensor(n_slots * slot_elems * esz, grad_dtype, ipc, device)
         self.grads = self.grads.view(n_slots, slot_elems)
-        self.params, self._p = region_tensor(slot_elems * 4, torch.float32, ipc, device)
+        # parameters share the gradient dtype (autograd requires it); bf16 models
+        # keep an fp32 master copy that only the update kernel touches
+        self.params, self._p = region_tensor(slot_elems * esz, grad_dtype, ipc, device)
+        self.master = (torch.empty(slot_elems, dtype=torch.float32, device=device)
+                       if grad_dtype == torch.bfloat16 else None)
         fbytes = int(_native.lib().deft_comm_flag_bytes(world))
         self.flags, self._f = region_tensor(fbytes, torch.uint8, ipc, device)
         self._opened: list[c_vp] = []
@@ -82,7 +86,8 @@ class BucketComm:
         arr = lambda xs: (c_vp * world)(*xs)  # noqa: E731
         h = c_vp()
         check(_native.lib().deft_comm_create(
-            rank, world, arr(maps.grads), arr(maps.params), arr(maps.flags), slot_elems, n_slots,
+            rank, world, arr(maps.grads), arr(maps.params), arr(maps.flags),
+            c_vp(self.master.data_ptr() if self.master is not None else None), slot_elems, n_slots,
             DTYPE_BF16 if grad_dtype == torch.bfloat16 else DTYPE_F32, ctypes.byref(h)),
             "deft_comm_create")
         self._h = h
@@ -119,6 +124,23 @@ class BucketComm:
                                                grad_scale, c_vp(mom.data_ptr()),
                                                c_vp(stream.cuda_stream)),
               "deft_bucket_update")
+
+    def update_local_multi(self, slot: int, ranges, scale: float, lr: float, momentum: float,
+                           mom: torch.Tensor, stream) -> None:
+        """W == 1: every bucket of one update event in ONE launch."""
+        if self.world != 1:
+            raise ValueError("update_local_multi is the single-rank path")
+        n = len(ranges)
+        offs = (ctypes.c_int64 * n)(*[lo for lo, _ in ranges])
+        lens = (ctypes.c_int64 * n)(*[hi - lo for lo, hi in ranges])
+        scales = (ctypes.c_float * n)(*([scale] * n))
+        esz = 2 if self.grad_dtype == torch.bfloat16 else 4
+        g = self._g.ptr.value + slot * self.slot_elems * esz
+        master = c_vp(self.master.data_ptr() if self.master is not None else None)
+        check(_native.lib().deft_sgd_momentum_update_multi(
+            c_vp(g), DTYPE_BF16 if self.grad_dtype == torch.bfloat16 else DTYPE_F32,
+            c_vp(self._p.ptr.value), master, c_vp(mom.data_ptr()), n, offs, lens, scales, lr,
+            momentum, c_vp(stream.cuda_stream)), "deft_sgd_momentum_update_multi")
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None:

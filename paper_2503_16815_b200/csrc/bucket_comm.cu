@@ -144,6 +144,29 @@ struct Vec<__nv_bfloat16> {
   __device__ static void put(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
 };
 
+// 4 consecutive elements <-> float4, for fp32 or bf16 storage
+__device__ __forceinline__ float4 load4(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+__device__ __forceinline__ float4 load4(const __nv_bfloat16* p) {
+  const uint2 r = *reinterpret_cast<const uint2*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+  const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ void store4(float* p, const float4& v) {
+  *reinterpret_cast<float4*>(p) = v;
+}
+__device__ __forceinline__ void store4(__nv_bfloat16* p, const float4& v) {
+  uint2 r;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&r);
+  h[0] = __floats2bfloat162_rn(v.x, v.y);
+  h[1] = __floats2bfloat162_rn(v.z, v.w);
+  *reinterpret_cast<uint2*>(p) = r;
+}
+__device__ __forceinline__ void store1(float* p, float v) { *p = v; }
+__device__ __forceinline__ void store1(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
 template <typename Raw>
 __device__ __forceinline__ Raw ld_nc(const Raw* p) {
   return __ldg(p);
@@ -320,23 +343,25 @@ __global__ void __launch_bounds__(kCommThreads) update_allgather_kernel(
     float scale, float* __restrict__ mom) {
   using V = Vec<T>;
   constexpr int U = 2;
+  constexpr bool kMaster = sizeof(T) == 2;  // bf16 params: fp32 master is authoritative
   // entry: every rank's no-read window for this bucket is open
   const uint32_t epoch = take_epochs(P, rank, kBarrierUpdate, 2u);
   peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 1u);
   const T* g = reinterpret_cast<const T*>(P.grads[rank]) + slot_base;
-  float* own = P.params[rank];
-  float* dst[W];
+  float* ref = kMaster ? P.master : reinterpret_cast<float*>(P.params[rank]);
+  T* dst[W];
 #pragma unroll
-  for (int k = 0; k < W; ++k) dst[k] = P.params[k];
+  for (int k = 0; k < W; ++k) dst[k] = reinterpret_cast<T*>(P.params[k]);
 
-  const Span s = split_span<4>(lo, hi);  // parameters are fp32: 4-element alignment
+  const Span s = split_span<4>(lo, hi);
   if (blockIdx.x == 0) {
     auto step = [&](int64_t e) {
       const float v = fmaf(momentum, mom[e], V::scalar(g + e) * scale);
       mom[e] = v;
-      const float p = fmaf(-lr, v, own[e]);
+      const float p = fmaf(-lr, v, ref[e]);
+      if (kMaster) ref[e] = p;
 #pragma unroll
-      for (int k = 0; k < W; ++k) dst[k][e] = p;
+      for (int k = 0; k < W; ++k) store1(dst[k] + e, p);
     };
     for (int64_t e = s.head_lo + threadIdx.x; e < s.head_hi; e += blockDim.x) step(e);
     for (int64_t e = s.tail_lo + threadIdx.x; e < s.tail_hi; e += blockDim.x) step(e);
@@ -345,24 +370,15 @@ __global__ void __launch_bounds__(kCommThreads) update_allgather_kernel(
   const int64_t v0 = s.body_lo / 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride * U) {
-    float gv[U][4];
-    float4 m4[U], p4[U];
+    float4 g4[U], m4[U], p4[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t vi = i + u * stride;
       if (vi < nv) {
         const int64_t e = (v0 + vi) * 4;
-        if constexpr (sizeof(T) == 4) {
-          const float4 r = __ldg(reinterpret_cast<const float4*>(g + e));
-          gv[u][0] = r.x; gv[u][1] = r.y; gv[u][2] = r.z; gv[u][3] = r.w;
-        } else {
-          const uint2 r = __ldg(reinterpret_cast<const uint2*>(g + e));
-          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
-          const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
-          gv[u][0] = a.x; gv[u][1] = a.y; gv[u][2] = b.x; gv[u][3] = b.y;
-        }
-        m4[u] = *reinterpret_cast<const float4*>(mom + e);
-        p4[u] = *reinterpret_cast<const float4*>(own + e);
+        g4[u] = load4(g + e);
+        m4[u] = load4(mom + e);
+        p4[u] = load4(ref + e);
       }
     }
 #pragma unroll
@@ -371,17 +387,18 @@ __global__ void __launch_bounds__(kCommThreads) update_allgather_kernel(
       if (vi < nv) {
         const int64_t e = (v0 + vi) * 4;
         float4 v4, q4;
-        v4.x = fmaf(momentum, m4[u].x, gv[u][0] * scale);
-        v4.y = fmaf(momentum, m4[u].y, gv[u][1] * scale);
-        v4.z = fmaf(momentum, m4[u].z, gv[u][2] * scale);
-        v4.w = fmaf(momentum, m4[u].w, gv[u][3] * scale);
+        v4.x = fmaf(momentum, m4[u].x, g4[u].x * scale);
+        v4.y = fmaf(momentum, m4[u].y, g4[u].y * scale);
+        v4.z = fmaf(momentum, m4[u].z, g4[u].z * scale);
+        v4.w = fmaf(momentum, m4[u].w, g4[u].w * scale);
         q4.x = fmaf(-lr, v4.x, p4[u].x);
         q4.y = fmaf(-lr, v4.y, p4[u].y);
         q4.z = fmaf(-lr, v4.z, p4[u].z);
         q4.w = fmaf(-lr, v4.w, p4[u].w);
-        *reinterpret_cast<float4*>(mom + e) = v4;
+        store4(mom + e, v4);
+        if (kMaster) store4(ref + e, q4);
 #pragma unroll
-        for (int k = 0; k < W; ++k) *reinterpret_cast<float4*>(dst[k] + e) = q4;
+        for (int k = 0; k < W; ++k) store4(dst[k] + e, q4);
       }
     }
   }
@@ -437,12 +454,21 @@ struct SegTable {
 
 template <typename T>
 __global__ void __launch_bounds__(kLocalThreads) sgd_local_kernel(
-    const T* __restrict__ grad, float* __restrict__ param, float* __restrict__ mom, SegTable t,
-    float lr, float momentum) {
+    const T* __restrict__ grad, T* __restrict__ param, float* __restrict__ master,
+    float* __restrict__ mom, SegTable t, float lr, float momentum) {
   using V = Vec<T>;
+  constexpr bool kMaster = sizeof(T) == 2;  // bf16 params: fp32 master is authoritative
+  float* ref = kMaster ? master : reinterpret_cast<float*>(param);
   const int64_t total = t.first_vec[t.count];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int seg = 0;
+  auto one = [&](int64_t e, float s) {
+    const float v = fmaf(momentum, mom[e], V::scalar(grad + e) * s);
+    mom[e] = v;
+    const float p = fmaf(-lr, v, ref[e]);
+    if (kMaster) ref[e] = p;
+    store1(param + e, p);
+  };
   for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < total; u += stride) {
     while (u >= t.first_vec[seg + 1]) ++seg;
     // unit u covers 4 consecutive elements of segment `seg`, from its aligned start
@@ -452,48 +478,32 @@ __global__ void __launch_bounds__(kLocalThreads) sgd_local_kernel(
     const int64_t k = u - t.first_vec[seg];
     const float s = t.scale[seg];
     if (k == 0 && aligned > base) {  // unit 0 also owns the unaligned head
-      for (int64_t e = base; e < aligned && e < end; ++e) {
-        const float v = fmaf(momentum, mom[e], V::scalar(grad + e) * s);
-        mom[e] = v;
-        param[e] = fmaf(-lr, v, param[e]);
-      }
+      for (int64_t e = base; e < aligned && e < end; ++e) one(e, s);
     }
     const int64_t e = aligned + k * 4;
     if (e + 4 <= end) {
-      float gv[4];
-      if constexpr (sizeof(T) == 4) {
-        const float4 r = __ldg(reinterpret_cast<const float4*>(grad + e));
-        gv[0] = r.x; gv[1] = r.y; gv[2] = r.z; gv[3] = r.w;
-      } else {
-        const uint2 r = __ldg(reinterpret_cast<const uint2*>(grad + e));
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
-        const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
-        gv[0] = a.x; gv[1] = a.y; gv[2] = b.x; gv[3] = b.y;
-      }
-      float4 m4 = *reinterpret_cast<const float4*>(mom + e);
-      float4 p4 = *reinterpret_cast<const float4*>(param + e);
-      m4.x = fmaf(momentum, m4.x, gv[0] * s);
-      m4.y = fmaf(momentum, m4.y, gv[1] * s);
-      m4.z = fmaf(momentum, m4.z, gv[2] * s);
-      m4.w = fmaf(momentum, m4.w, gv[3] * s);
+      const float4 g4 = load4(grad + e);
+      float4 m4 = load4(mom + e);
+      float4 p4 = load4(ref + e);
+      m4.x = fmaf(momentum, m4.x, g4.x * s);
+      m4.y = fmaf(momentum, m4.y, g4.y * s);
+      m4.z = fmaf(momentum, m4.z, g4.z * s);
+      m4.w = fmaf(momentum, m4.w, g4.w * s);
       p4.x = fmaf(-lr, m4.x, p4.x);
       p4.y = fmaf(-lr, m4.y, p4.y);
       p4.z = fmaf(-lr, m4.z, p4.z);
       p4.w = fmaf(-lr, m4.w, p4.w);
-      *reinterpret_cast<float4*>(mom + e) = m4;
-      *reinterpret_cast<float4*>(param + e) = p4;
+      store4(mom + e, m4);
+      if (kMaster) store4(ref + e, p4);
+      store4(param + e, p4);
     } else {
-      for (int64_t x = e; x < end; ++x) {  // tail
-        const float v = fmaf(momentum, mom[x], V::scalar(grad + x) * s);
-        mom[x] = v;
-        param[x] = fmaf(-lr, v, param[x]);
-      }
+      for (int64_t x = e; x < end; ++x) one(x, s);  // tail
     }
   }
 }
 
-cudaError_t launch_sgd_local(const void* grad, int dtype, float* param, float* mom,
-                             int32_t count, const int64_t* offsets, const int64_t* numels,
+cudaError_t launch_sgd_local(const void* grad, int dtype, void* param, float* master,
+                             float* mom, int32_t count, const int64_t* offsets, const int64_t* numels,
                              const float* scales, float lr, float momentum,
                              cudaStream_t stream) {
   for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
@@ -516,10 +526,12 @@ cudaError_t launch_sgd_local(const void* grad, int dtype, float* param, float* m
     if (grid > 148 * 8) grid = 148 * 8;
     if (dtype == 0)
       sgd_local_kernel<float><<<(int)grid, kLocalThreads, 0, stream>>>(
-          reinterpret_cast<const float*>(grad), param, mom, t, lr, momentum);
+          reinterpret_cast<const float*>(grad), reinterpret_cast<float*>(param), nullptr, mom, t,
+          lr, momentum);
     else
       sgd_local_kernel<__nv_bfloat16><<<(int)grid, kLocalThreads, 0, stream>>>(
-          reinterpret_cast<const __nv_bfloat16*>(grad), param, mom, t, lr, momentum);
+          reinterpret_cast<const __nv_bfloat16*>(grad), reinterpret_cast<__nv_bfloat16*>(param),
+          master, mom, t, lr, momentum);
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -328,13 +328,16 @@ extern "C" size_t deft_comm_flag_bytes(int32_t world) {
 
 extern "C" deft_status_t deft_comm_create(int32_t rank, int32_t world, void* const* grads,
                                           void* const* params, void* const* flags,
-                                          int64_t slot_elems, int32_t n_slots,
+                                          float* d_master, int64_t slot_elems, int32_t n_slots,
                                           int32_t grad_dtype, deft_comm** out) {
   if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world || !out)
     return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_comm_create: bad rank/world");
   if (grad_dtype != DEFT_DTYPE_F32 && grad_dtype != DEFT_DTYPE_BF16)
     return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_comm_create: bad dtype");
+  if (grad_dtype == DEFT_DTYPE_BF16 && !d_master)
+    return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_comm_create: bf16 parameters need an fp32 master");
   deft_comm* c = new deft_comm();
+  c->P.master = grad_dtype == DEFT_DTYPE_BF16 ? d_master : nullptr;
   c->rank = rank;
   c->world = world;
   c->dtype = grad_dtype;
@@ -342,7 +345,7 @@ extern "C" deft_status_t deft_comm_create(int32_t rank, int32_t world, void* con
   c->n_slots = n_slots;
   for (int r = 0; r < world; ++r) {
     c->P.grads[r] = reinterpret_cast<char*>(grads[r]);
-    c->P.params[r] = reinterpret_cast<float*>(params[r]);
+    c->P.params[r] = params[r];
     c->P.flags[r] = flags ? reinterpret_cast<uint32_t*>(flags[r]) : nullptr;
     if (world > 1 && !c->P.flags[r]) {
       delete c;
@@ -429,8 +432,8 @@ extern "C" deft_status_t deft_bucket_update(deft_comm* c, int32_t slot, int64_t 
   if (c->world == 1) {
     const int esz = c->dtype == DEFT_DTYPE_F32 ? 4 : 2;
     const char* g = c->P.grads[0] + slot_base * esz;
-    cudaError_t e = launch_sgd_local(g, c->dtype, c->P.params[0], d_mom, 1, &offset, &numel,
-                                     &grad_scale, lr, momentum, s);
+    cudaError_t e = launch_sgd_local(g, c->dtype, c->P.params[0], c->P.master, d_mom, 1,
+                                     &offset, &numel, &grad_scale, lr, momentum, s);
     if (e != cudaSuccess) return cuda_fail(e, "sgd_local_kernel");
     return DEFT_OK;
   }
@@ -441,26 +444,31 @@ extern "C" deft_status_t deft_bucket_update(deft_comm* c, int32_t slot, int64_t 
 }
 
 extern "C" deft_status_t deft_sgd_momentum_update(const void* d_grad, int32_t grad_dtype,
-                                                  float* d_param, float* d_mom, int64_t numel,
-                                                  float lr, float momentum, float grad_scale,
-                                                  void* stream) {
+                                                  void* d_param, float* d_master, float* d_mom,
+                                                  int64_t numel, float lr, float momentum,
+                                                  float grad_scale, void* stream) {
   if (numel == 0) return DEFT_OK;
+  if (grad_dtype == DEFT_DTYPE_BF16 && !d_master)
+    return fail(DEFT_ERR_INVALID_ARGUMENT, "bf16 parameters need an fp32 master");
   int64_t off = 0;
-  cudaError_t e = launch_sgd_local(d_grad, grad_dtype, d_param, d_mom, 1, &off, &numel,
+  cudaError_t e = launch_sgd_local(d_grad, grad_dtype, d_param, d_master, d_mom, 1, &off, &numel,
                                    &grad_scale, lr, momentum, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "sgd_local_kernel");
   return DEFT_OK;
 }
 
 extern "C" deft_status_t deft_sgd_momentum_update_multi(const void* d_grad, int32_t grad_dtype,
-                                                        float* d_param, float* d_mom,
-                                                        int32_t count, const int64_t* offsets,
+                                                        void* d_param, float* d_master,
+                                                        float* d_mom, int32_t count,
+                                                        const int64_t* offsets,
                                                         const int64_t* numels,
                                                         const float* grad_scales, float lr,
                                                         float momentum, void* stream) {
   if (count <= 0) return DEFT_OK;
-  cudaError_t e = launch_sgd_local(d_grad, grad_dtype, d_param, d_mom, count, offsets, numels,
-                                   grad_scales, lr, momentum, (cudaStream_t)stream);
+  if (grad_dtype == DEFT_DTYPE_BF16 && !d_master)
+    return fail(DEFT_ERR_INVALID_ARGUMENT, "bf16 parameters need an fp32 master");
+  cudaError_t e = launch_sgd_local(d_grad, grad_dtype, d_param, d_master, d_mom, count, offsets,
+                                   numels, grad_scales, lr, momentum, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "sgd_local_kernel");
   return DEFT_OK;
 }

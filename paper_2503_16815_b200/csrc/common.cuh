@@ -41,8 +41,9 @@ enum BarrierSet : int { kBarrierRS = 0, kBarrierCE = 1, kBarrierUpdate = 2, kNum
 
 struct PeerPtrs {
   char* grads[kMaxWorld];
-  float* params[kMaxWorld];
+  void* params[kMaxWorld];   // same dtype as the gradients (fp32 or bf16)
   uint32_t* flags[kMaxWorld];
+  float* master;             // this rank's fp32 master copy when params are bf16, else null
 };
 
 struct ShardRange {
@@ -78,8 +79,8 @@ cudaError_t launch_update_allgather(const PeerPtrs& P, int rank, int world, int 
                                     int64_t slot_base, int64_t offset, int64_t numel, float lr,
                                     float momentum, float grad_scale, float* mom,
                                     cudaStream_t stream);
-cudaError_t launch_sgd_local(const void* grad, int dtype, float* param, float* mom,
-                             int32_t count, const int64_t* offsets, const int64_t* numels,
+cudaError_t launch_sgd_local(const void* grad, int dtype, void* param, float* master,
+                             float* mom, int32_t count, const int64_t* offsets, const int64_t* numels,
                              const float* scales, float lr, float momentum,
                              cudaStream_t stream);
 

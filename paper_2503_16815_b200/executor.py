@@ -62,6 +62,10 @@ class DeftConfig:
     use_ce_channel: bool = True             # second link = copy engines
     instrument: bool = False                # CUDA events around every native launch
     cuda_graphs: bool = True                # capture + replay each distinct iteration shape
+    # where the delayed update of bucket b runs inside its no-read window:
+    # "bucket" = right after b's backward (overlaps the rest of the backward),
+    # "end" = after the whole backward (one launch per event at W == 1)
+    update_placement: str = "bucket"
     graph_warmup: int = 1                   # eager runs of a shape before it is captured
 
 
@@ -90,6 +94,12 @@ class DeftDataParallel:
         self.params = [p for p in module.parameters() if p.requires_grad][::-1]
         self.numels = [p.numel() for p in self.params]
         self.total = sum(self.numels)
+        dtypes = {p.dtype for p in self.params}
+        if len(dtypes) != 1 or next(iter(dtypes)) not in (torch.float32, torch.bfloat16):
+            raise DeftError(f"parameters must all be fp32 or all bf16, got {dtypes}")
+        # gradients (and the symmetric parameter copies) carry the parameter dtype;
+        # bf16 models get an fp32 master inside the update kernel
+        self.cfg.grad_dtype = next(iter(dtypes))
         self.comm = BucketComm(self.rank, self.world, self.cfg.n_slots, self.total,
                                self.cfg.grad_dtype, self.device, process_group)
         self.mom = torch.zeros(self.total, dtype=torch.float32, device=self.device)
@@ -124,6 +134,8 @@ class DeftDataParallel:
                 off += n
             if self.world > 1:
                 torch.distributed.broadcast(flat, src=0, group=self.group)
+            if self.comm.master is not None:
+                self.comm.master.copy_(flat.float())
         torch.cuda.synchronize(self.device)
         self._grad_views = []
         for s in range(self.cfg.n_slots):
@@ -398,6 +410,25 @@ class DeftDataParallel:
                                              self.cfg.momentum, 1.0 / (self.world * k),
                                              self.mom, s), nbytes)
 
+    def _updates_at_end(self, comp):
+        """All due updates after the whole backward (every no-read window is open):
+        one multi-bucket launch per group on the compute stream at W == 1; per
+        bucket update + all-gather kernels on the update stream at W > 1."""
+        if self.world == 1:
+            ranges = [(b.lo, b.hi) for b in self.buckets]
+            esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
+            nbytes = self.total * 20  # read g, v, p(master); write v, p (+bf16 copy)
+            for slot, k in self._due_now:
+                self._timed("update", comp, lambda: self.comm.update_local_multi(
+                    slot, ranges, 1.0 / k, self.cfg.lr, self.cfg.momentum, self.mom, comp),
+                    nbytes)
+            return
+        ev = torch.cuda.Event()
+        ev.record(comp)
+        for slot, k in self._due_now:
+            for bidx in range(len(self.buckets)):
+                self._issue_update(slot, k, bidx, ev)
+
     def _on_grad(self, p):
         if not self._in_step:
             return
@@ -412,8 +443,9 @@ class DeftDataParallel:
         ev.record(torch.cuda.current_stream(self.device))
         for link, slot in self._fresh_now.pop(bidx, ()):
             self._issue_rs(link, slot, bidx, ev)
-        for slot, k in self._due_now:
-            self._issue_update(slot, k, bidx, ev)
+        if self.cfg.update_placement == "bucket":
+            for slot, k in self._due_now:
+                self._issue_update(slot, k, bidx, ev)
         self._fired[bidx] = True
 
     def _run_iteration(self, it: IterPlan, batch, loss_fn: Callable) -> torch.Tensor:
@@ -450,6 +482,8 @@ class DeftDataParallel:
         for b in range(len(self.buckets)):      # buckets whose params got no gradient
             if not self._fired[b]:
                 self._bucket_ready(b)
+        if self.cfg.update_placement == "end" and self._due_now:
+            self._updates_at_end(comp)
         if self._fresh_now:
             raise InternalInvariantError("fresh transfers left unreleased")
         loss = loss.detach()  # drop the autograd graph (no stale AccumulateGrad nodes)

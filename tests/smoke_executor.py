@@ -47,6 +47,13 @@ def flat_grad(total, rank, t, seed=11):
     return torch.randn(total, generator=g)
 
 
+def flat_grad_dyadic(total, rank, t, seed=13):
+    """Small multiples of 1/16: exact in bf16, and so are sums of a few of them
+    (merges accumulate in the bf16 slot; the reduce-scatter rounds to bf16)."""
+    g = torch.Generator().manual_seed(seed * 1_000_003 + 7919 * t + rank)
+    return torch.randint(-8, 9, (total,), generator=g).float() / 16
+
+
 def uniform_profile(n, param_count, comm_us=900, fwd_total=3600, bwd_total=7200):
     fwd = [fwd_total // n] * n
     bwd = [bwd_total // n] * n
@@ -65,10 +72,12 @@ def equal_dual():
 
 
 def run_executor(world, rank, iterations, n_buckets=48, total=48_000, lr=0.05, momentum=0.9,
-                 grad_dtype=torch.float32, comm_us=900, group=None, cuda_graphs=True):
-    """Run the executor on the probe; return (theta^(T) flat CPU, decisions as dicts)."""
-    model = Probe(probe_sizes(total)).cuda()
-    cfg = D.DeftConfig(lr=lr, momentum=momentum, autocast_dtype=None, grad_dtype=grad_dtype,
+                 dtype=torch.float32, comm_us=900, group=None, cuda_graphs=True,
+                 grad_fn=flat_grad):
+    """Run the executor on the probe; return (theta^(T) flat fp32 CPU -- the fp32
+    master for bf16 models --, theta0, decisions as dicts[, bf16 params])."""
+    model = Probe(probe_sizes(total)).cuda().to(dtype)
+    cfg = D.DeftConfig(lr=lr, momentum=momentum, autocast_dtype=None,
                        partition=D.PartitionConfig(partition_size=10**9),
                        cuda_graphs=cuda_graphs)
     ddp = D.DeftDataParallel(model, cfg, process_group=group)
@@ -80,20 +89,25 @@ def run_executor(world, rank, iterations, n_buckets=48, total=48_000, lr=0.05, m
         return module(batch)
 
     for t in range(iterations):
-        flat = flat_grad(total, rank, t).cuda()
+        flat = grad_fn(total, rank, t).cuda().to(dtype)
         xs_exec = [flat[o:o + p.numel()].view_as(p) for o, p in zip(ddp.offsets, order)]
         ddp.train_step(xs_exec[::-1], loss_fn)
     ddp.finish()
-    theta = ddp.comm.params.detach().float().cpu().clone()
+    master = ddp.comm.master if ddp.comm.master is not None else ddp.comm.params
+    theta = master.detach().float().cpu().clone()
+    params = ddp.comm.params.detach().cpu().clone()
     decisions = [d.to_dict() for k in range(iterations) for d in ddp.decisions(k)]
-    theta0 = torch.cat([p.detach().float().reshape(-1) for p in
+    theta0 = torch.cat([p.detach().to(dtype).float().reshape(-1) for p in
                         Probe(probe_sizes(total)).ps][::-1])
     ddp.close()
+    if dtype == torch.bfloat16:
+        return theta, theta0, decisions, params
     return theta, theta0, decisions
 
 
-def oracle_theta(theta0, decisions, world, iterations, total=48_000, lr=0.05, momentum=0.9):
-    return delayed_sgd.run(theta0, lambda th, r, t: flat_grad(total, r, t), decisions, world,
+def oracle_theta(theta0, decisions, world, iterations, total=48_000, lr=0.05, momentum=0.9,
+                 grad_fn=flat_grad):
+    return delayed_sgd.run(theta0, lambda th, r, t: grad_fn(total, r, t), decisions, world,
                            lr, momentum, iterations)
 
 

@@ -26,6 +26,19 @@ def test_single_gpu_matches_oracle(iterations, comm_us, graphs):
     assert S.rel_err(theta, want) <= S.TOL
 
 
+@pytest.mark.parametrize("graphs", [True, False])
+def test_bf16_params_single_gpu(graphs):
+    """bf16 model (bf16 grads, as the GPT-2 config): the fp32 master follows the
+    oracle within 1e-6 and the bf16 parameters are its round-to-nearest copy."""
+    iters = 16
+    theta, theta0, decisions, params = S.run_executor(
+        1, 0, iters, dtype=torch.bfloat16, cuda_graphs=graphs, grad_fn=S.flat_grad_dyadic)
+    assert max(u["merge_count"] for d in decisions for u in d["update_events"]) >= 2
+    want = S.oracle_theta(theta0, decisions, 1, iters, grad_fn=S.flat_grad_dyadic)
+    assert S.rel_err(theta, want) <= S.TOL
+    assert torch.equal(params, theta.bfloat16())
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -34,16 +47,22 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, iterations, comm_us, graphs, q):
+def _worker(rank, world, port, iterations, comm_us, graphs, q, bf16=False):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world,
                             device_id=torch.device("cuda", rank))
     try:
-        theta, theta0, decisions = S.run_executor(world, rank, iterations, comm_us=comm_us,
-                                                  cuda_graphs=graphs)
-        q.put((rank, theta, theta0, decisions))
+        if bf16:
+            theta, theta0, decisions, params = S.run_executor(
+                world, rank, iterations, comm_us=comm_us, cuda_graphs=graphs,
+                dtype=torch.bfloat16, grad_fn=S.flat_grad_dyadic)
+            q.put((rank, theta, theta0, decisions, params))
+        else:
+            theta, theta0, decisions = S.run_executor(world, rank, iterations, comm_us=comm_us,
+                                                      cuda_graphs=graphs)
+            q.put((rank, theta, theta0, decisions))
     finally:
         dist.destroy_process_group()
 
@@ -76,3 +95,50 @@ def test_multi_gpu_matches_oracle(iterations, comm_us, graphs):
         assert res[r][2] == decisions          # every rank planned the same stream
         assert S.rel_err(res[r][0], want) <= S.TOL, r
         assert torch.equal(res[r][0], res[0][0])  # replicas bit-identical
+
+
+def shard_range(offset, numel, r, world, align):
+    """Python copy of shard_of() (csrc/common.cuh)."""
+    per = (numel + world - 1) // world
+
+    def bound(k):
+        if k <= 0:
+            return offset
+        if k >= world:
+            return offset + numel
+        b = -(-(offset + k * per) // align) * align
+        return min(b, offset + numel)
+    return bound(r), bound(r + 1)
+
+
+@pytest.mark.multigpu
+def test_multi_gpu_bf16_matches_oracle():
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world, iterations = min(n, 4), 14
+    ctx = torch.multiprocessing.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, iterations, 900, True, q, True))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, theta, theta0, decisions, params = q.get(timeout=300)
+        res[r] = (theta, theta0, decisions, params)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    theta0, decisions = res[0][1], res[0][2]
+    want = S.oracle_theta(theta0, decisions, world, iterations, grad_fn=S.flat_grad_dyadic)
+    for r in range(world):
+        theta, _, dec, params = res[r]
+        assert dec == decisions
+        assert torch.equal(params, res[0][3])        # every rank holds the same bf16 params
+        for b in range(48):                          # uniform48 probe buckets of 1000
+            lo, hi = shard_range(1000 * b, 1000, r, world, 8)
+            # the owner's fp32 master shard follows the oracle within 1e-6
+            assert S.rel_err(theta[lo:hi], want[lo:hi]) <= S.TOL, (r, b)
+            assert torch.equal(params[lo:hi], theta[lo:hi].bfloat16())
