@@ -25,6 +25,9 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# rank 0 prints exactly ONE JSON line on stdout: keep NCCL's version banner off it
+if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
 
 BATCH = 64
 METRIC = "samples/sec (DeFT delayed-update DP training step)"
@@ -36,11 +39,18 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--model", default="resnet101", choices=["resnet101", "vgg19", "gpt2"])
-    ap.add_argument("--impl", default="deft", choices=["deft", "reference"])
+    ap.add_argument("--impl", default="deft", choices=["deft", "reference", "ddp"],
+                    help="deft (this repo), reference (CPU oracle port), ddp (PyTorch DDP + "
+                         "NCCL WFBP baseline)")
     ap.add_argument("--batch", type=int, default=None,
                     help="per-GPU batch (default 64; GPT-2: 16 sequences of 1024)")
-    ap.add_argument("--update-placement", default="bucket", choices=["bucket", "end"])
+    ap.add_argument("--update-placement", default="end", choices=["bucket", "end"])
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs")
+    ap.add_argument("--bucket-mb", type=float, default=None,
+                    help="partition size in MB of fp32 (default: the reference's 6.5M params)")
+    ap.add_argument("--comm-scale", type=float, default=1.0,
+                    help="scale the measured comm times before planning (slower-link / "
+                         "update-frequency sweep: >1 makes DeFT merge iterations)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -287,12 +297,12 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
 
     saved_p = ddp.comm.params.clone()
     saved_m = ddp.mom.clone()
-    if ddp.cfg.grad_dtype == torch.bfloat16:   # g 2 + v 8 + master 8 + bf16 p to W ranks
+    if ddp.cfg.grad_dtype == torch.bfloat16:
         esz = 2
-        per = lambda w: 2 + 16 + 2 * w  # noqa: E731
-    else:                                     # g 4 + v 8 + p 8 (+4 per extra rank)
-        per = lambda w: 4 + 16 + 4 * (w - 1)  # noqa: E731
-    upd_bytes = sum(((b.hi - b.lo + world - 1) // world) * per(world) for b in ddp.buckets)
+    if world == 1:      # HBM bytes: read g, v, p (master); write v, p (+ bf16 copy)
+        upd_bytes = sum((b.hi - b.lo) * 20 for b in ddp.buckets)
+    else:               # NVLink bytes: updated params stored to the W-1 peers
+        upd_bytes = sum((b.hi - b.lo) * esz * (world - 1) // world for b in ddp.buckets)
 
     def updates():
         for b in ddp.buckets:
@@ -311,6 +321,58 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
     ddp.mom.copy_(saved_m)
     torch.cuda.synchronize()
     return out
+
+
+def ddp_baseline(args, world, rank, device, dist):
+    """NCCL WFBP baseline: torch DistributedDataParallel (bucketed all-reduce
+    overlapped with backward, every iteration) + fused SGD/momentum, eager."""
+    import torch
+    model = build_model(args.model, device)
+    loss_fn = loss_fn_for(args.model)
+    batch = make_batch(args.model, args.batch, device, seed=1234 + rank)
+    bucket_mb = args.bucket_mb or 25
+    net = model
+    if world > 1:
+        net = torch.nn.parallel.DistributedDataParallel(model, device_ids=[device.index],
+                                                        bucket_cap_mb=bucket_mb,
+                                                        gradient_as_bucket_view=True)
+    opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9, fused=True)
+    amp = next(model.parameters()).dtype == torch.float32
+
+    def step():
+        opt.zero_grad(set_to_none=False)
+        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=amp):
+            loss = loss_fn(net, batch)
+        loss.backward()
+        opt.step()
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        step()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({
+            "impl": "ddp", "metric": METRIC, "value": round(args.batch * world * args.steps /
+                                                          (ms / 1e3), 2),
+            "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "dtype": "bf16",
+            "config": {"workload": f"{args.model} torch DDP (NCCL all-reduce WFBP) + fused SGD, "
+                                   f"batch {args.batch}/GPU", "bucket_cap_mb": bucket_mb}}))
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
@@ -345,6 +407,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
     torch.backends.cudnn.benchmark = True
+    if args.impl == "ddp":
+        return ddp_baseline(args, world, rank, device, dist)
     import paper_2503_16815_b200 as D
 
     model = build_model(args.model, device)
@@ -358,14 +422,17 @@ def main():
     # 2) DeFT: profile on this GPU, plan (partition + feedback loop), run
     walk = D.WalkParams.from_dict(
         json.loads((ROOT / "tests" / "golden" / "inputs.json").read_text())["walk"])
+    psize = 6_500_000 if args.bucket_mb is None else int(args.bucket_mb * 2**20 / 4)
     cfg = D.DeftConfig(lr=0.1, momentum=0.9, walk=walk, cuda_graphs=not args.eager,
                        update_placement=args.update_placement,
                        autocast_dtype=None if args.model == "gpt2" else torch.bfloat16,
-                       partition=D.PartitionConfig(partition_size=6_500_000, mu=1.0))
+                       partition=D.PartitionConfig(partition_size=psize, mu=1.0))
     ddp = D.DeftDataParallel(model, cfg)
     t_setup = time.perf_counter()
-    ddp.measure_profile(batch, loss_fn, iters=3, name=args.model, batch_size=args.batch)
-    part = ddp.plan()
+    prof = ddp.measure_profile(batch, loss_fn, iters=3, name=args.model, batch_size=args.batch)
+    if args.comm_scale != 1.0:
+        prof = prof.scaled_comm(args.comm_scale)
+    part = ddp.plan(prof, ddp.cluster)
     t_setup = time.perf_counter() - t_setup
 
     def timed(step_fn, k):
@@ -396,24 +463,44 @@ def main():
     ms_step = ms / args.steps
     value = args.batch * world * args.steps / (ms / 1e3)
 
-    # 3) e2e: inputs from pinned host memory each step, loss read back each step
+    # 3) e2e: every step's inputs copied from pinned host memory (on a copy stream,
+    #    double-buffered so the copy for step t+1 overlaps step t) and every step's
+    #    loss read back to pinned host memory
     hx = batch[0].cpu().pin_memory()
     hy = batch[1].cpu().pin_memory()
     loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
-    dx, dy = batch if ddp.static_batch is not None else (torch.empty_like(batch[0]),
-                                                         torch.empty_like(batch[1]))
+    copy_stream = torch.cuda.Stream(device)
+    staging = [(torch.empty_like(batch[0]), torch.empty_like(batch[1])) for _ in range(2)]
+    loaded = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+    state = {"i": 0}
+
+    def h2d(k):
+        copy_stream.wait_event(consumed[k])
+        with torch.cuda.stream(copy_stream):
+            staging[k][0].copy_(hx, non_blocking=True)
+            staging[k][1].copy_(hy, non_blocking=True)
+        loaded[k].record(copy_stream)
+
+    for k in range(2):
+        consumed[k].record()
+    h2d(0)
 
     def e2e_step():
-        dx.copy_(hx, non_blocking=True)
-        dy.copy_(hy, non_blocking=True)
-        loss = ddp.train_step((dx, dy), loss_fn)
+        i = state["i"]
+        cur, nxt = i % 2, (i + 1) % 2
+        h2d(nxt)                                   # next step's inputs, overlapped
+        torch.cuda.current_stream().wait_event(loaded[cur])
+        loss = ddp.train_step(staging[cur], loss_fn)
+        consumed[cur].record()
         loss_host.copy_(loss.float().reshape(1), non_blocking=True)
+        state["i"] = i + 1
 
     for _ in range(2):
         e2e_step()
     ms_e2e = timed(e2e_step, args.steps)
     e2e_value = args.batch * world * args.steps / (ms_e2e / 1e3)
-    h2d = hx.numel() * hx.element_size() + hy.numel() * hy.element_size()
+    h2d_bytes = hx.numel() * hx.element_size() + hy.numel() * hy.element_size()
 
     # 4) kernel roofline: (a) in-step -- an instrumented eager pass with CUDA events
     #    around every native launch on its own stream; (b) isolated, barrier-aligned
@@ -444,9 +531,10 @@ def main():
             "in_step_achieved": round(in_step, 1) if in_step else None,
             "in_step_note": "same kernel inside the training step (overlapping backward "
                             "compute; at W>1 includes cross-rank barrier waits)",
-            "algorithmic_bytes": "update: 20 B/param (W=1: read g,v,p; write v,p); "
-                                 "W>1 per owned elem 16 B + 4 B per rank of p; "
-                                 "reduce-scatter: (W-1)/W x bucket bytes crossing NVLink",
+            "algorithmic_bytes": "W=1 update: 20 B/param of HBM traffic (read g,v,p; write v,p). "
+                                 "W>1: bytes crossing NVLink per rank = (W-1)/W x bucket "
+                                 "bytes, for the reduce-scatter (peer loads) and for the "
+                                 "update+all-gather (peer stores) alike",
             "peak_src": (pk["src"] + " MEASURED_PEAKS.json hbm_gbs") if hbm_bound
             else "B200_PROFILING.md measured peer copy 770 GB/s",
             "isolated": iso, "in_step": ks}
@@ -474,9 +562,14 @@ def main():
                        "update_placement": ddp.cfg.update_placement,
                        "buckets": part.n_buckets, "links": [l.name for l in ddp.cluster.links],
                        "capacity_multiplier": ddp.capacity_multiplier,
+                       "partition_size": psize, "comm_scale": args.comm_scale,
+                       "merge_counts": sorted({u.merge_count for pair in ddp.decision_log
+                                               for d in pair for u in d.update_events}),
                        "cuda_graphs": ddp.cfg.cuda_graphs, "setup_s": round(t_setup, 2)},
             "e2e": {"value": round(e2e_value, 2), "unit": "samples/s",
-                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4},
+                    "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": 4,
+                    "note": "H2D on a copy stream, double-buffered (copy of step t+1 "
+                            "overlaps step t); loss D2H every step"},
             "gpu_launches": int(launches),
             "compute_only_ms_per_step": round(ms_compute, 3),
             "exposed_comm_ms": round(ms_step - ms_compute, 3),

@@ -65,7 +65,7 @@ class DeftConfig:
     # where the delayed update of bucket b runs inside its no-read window:
     # "bucket" = right after b's backward (overlaps the rest of the backward),
     # "end" = after the whole backward (one launch per event at W == 1)
-    update_placement: str = "bucket"
+    update_placement: str = "end"
     graph_warmup: int = 1                   # eager runs of a shape before it is captured
 
 
@@ -385,7 +385,7 @@ class DeftDataParallel:
         s.wait_event(release)
         self._touched[id(s)] = s
         esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
-        nbytes = (b.hi - b.lo) * esz * (self.world - 1) // self.world * 2
+        nbytes = (b.hi - b.lo) * esz * (self.world - 1) // self.world  # crossing NVLink
         self._timed("reduce_scatter", s,
                     lambda: self.comm.reduce_scatter(self.channel_of_link[link], slot, b.lo,
                                                      b.hi - b.lo, s), nbytes)
@@ -403,8 +403,10 @@ class DeftDataParallel:
         if rs is not None:
             s.wait_event(rs)
         esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
-        shard = (b.hi - b.lo + self.world - 1) // self.world
-        nbytes = shard * (esz + 4 * 4) + shard * 4 * (self.world - 1)
+        if self.world == 1:   # HBM: read g, v, p; write v, p
+            nbytes = (b.hi - b.lo) * 20
+        else:                 # NVLink: the owned shard's new params stored to W-1 peers
+            nbytes = (b.hi - b.lo) * esz * (self.world - 1) // self.world
         self._timed("update", s,
                     lambda: self.comm.update(slot, b.lo, b.hi - b.lo, self.cfg.lr,
                                              self.cfg.momentum, 1.0 / (self.world * k),
