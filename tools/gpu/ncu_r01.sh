@@ -1,5 +1,6 @@
 # ncu evidence, 1 GPU. Every ncu command runs only after the same command exited 0 without ncu.
 set -x
+timeout 600 python bench.py > gpurun_out/bench9_n1.json 2> gpurun_out/bench9_n1.err; echo bench rc=$?; cat gpurun_out/bench9_n1.json
 python tools/profile_step.py > gpurun_out/prof_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
     --log-file gpurun_out/ncu_launches_step.csv python tools/profile_step.py > gpurun_out/ncu_launch_run.log 2>&1
