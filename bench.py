@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs")
     ap.add_argument("--bucket-mb", type=float, default=None,
                     help="partition size in MB of fp32 (default: the reference's 6.5M params)")
+    ap.add_argument("--dump-profile", default=None,
+                    help="write the B200-measured ModelProfile + ClusterSpec JSON here")
     ap.add_argument("--comm-scale", type=float, default=1.0,
                     help="scale the measured comm times before planning (slower-link / "
                          "update-frequency sweep: >1 makes DeFT merge iterations)")
@@ -290,7 +292,8 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
             t = torch.tensor([ms], device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        n = len(ddp.buckets)
+        n = 1 if (kind == "update" and world == 1 and ddp.cfg.update_placement == "end") \
+            else len(ddp.buckets)
         out[kind] = {"launches": n, "ms_per_pass": round(ms, 4),
                      "avg_launch_us": round(ms / n * 1e3, 2), "bytes_per_pass": nbytes,
                      "achieved_gbs": round(nbytes / (ms / 1e3) / 1e9, 1)}
@@ -305,6 +308,10 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
         upd_bytes = sum((b.hi - b.lo) * esz * (world - 1) // world for b in ddp.buckets)
 
     def updates():
+        if world == 1 and ddp.cfg.update_placement == "end":   # the step's own launch shape
+            ddp.comm.update_local_multi(slot, [(b.lo, b.hi) for b in ddp.buckets], 1.0, 0.0,
+                                        0.9, ddp.mom, s)
+            return
         for b in ddp.buckets:
             ddp.comm.update(slot, b.lo, b.hi - b.lo, 0.0, 0.9, 1.0, ddp.mom, s)
     with torch.cuda.stream(s):
@@ -430,6 +437,10 @@ def main():
     ddp = D.DeftDataParallel(model, cfg)
     t_setup = time.perf_counter()
     prof = ddp.measure_profile(batch, loss_fn, iters=3, name=args.model, batch_size=args.batch)
+    if args.dump_profile and rank == 0:
+        Path(args.dump_profile).write_text(json.dumps(
+            {"profile": D.profile_to_dict(prof), "cluster": D.cluster_to_dict(ddp.cluster)},
+            indent=1, sort_keys=True))
     if args.comm_scale != 1.0:
         prof = prof.scaled_comm(args.comm_scale)
     part = ddp.plan(prof, ddp.cluster)

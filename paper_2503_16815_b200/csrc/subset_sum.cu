@@ -7,7 +7,7 @@
 // are built from the highest id down (knapsack.py:72-78).  The working row
 // lives in shared memory when it fits (<= kSmemWords words, i.e. capacities
 // up to ~1.8M us -- every fixture configuration) and is updated IN PLACE,
-// top-down in chunks of one word per thread: word j of the new row reads only
+// top-down in chunks of 4 words per thread: word j of the new row reads only
 // words <= j of the old row, so after the chunk's loads a single
 // __syncthreads() makes the stores safe, and lower chunks never read the
 // stored words.  Every changed row is also streamed to global memory because
@@ -27,6 +27,7 @@
 namespace deft {
 
 constexpr int kSubsetThreads = 1024;
+constexpr int kWordsPerThread = 4;  // words per thread per in-place chunk
 constexpr int64_t kSmemWords = 56 * 1024;  // 224 KiB working row
 
 struct SubsetSumArgs {
@@ -104,21 +105,31 @@ __global__ void __launch_bounds__(kSubsetThreads, 1) subset_sum_kernel(SubsetSum
     const uint32_t* src = kSmem ? smem_row : rows + (int64_t)cur_slot * words;
     uint32_t* gdst = rows + (int64_t)i * words;
     const bool store_global = kSmem ? (i >= 1) : true;  // S[0] is only scanned for best
-    for (int64_t top = hi_new; top >= 0; top -= kSubsetThreads) {
-      const int64_t j = top - tid;
-      uint32_t v = 0;
-      if (j >= 0) {
-        const uint32_t cur = (j <= hi_old) ? src[j] : 0u;
-        const int64_t js = j - qw;
-        const uint32_t hi = (js >= 0 && js <= hi_old) ? src[js] : 0u;
-        const uint32_t lo = (js >= 1 && js - 1 <= hi_old) ? src[js - 1] : 0u;
-        v = cur | __funnelshift_l(lo, hi, r);
-        if (j == words - 1) v &= last_mask;
+    // chunks of kWordsPerThread * 1024 words, top-down; thread t owns words
+    // top - t - k*1024 (k < kWordsPerThread) so every pass stays coalesced
+    for (int64_t top = hi_new; top >= 0; top -= kSubsetThreads * kWordsPerThread) {
+      uint32_t v[kWordsPerThread];
+#pragma unroll
+      for (int k = 0; k < kWordsPerThread; ++k) {
+        const int64_t j = top - tid - (int64_t)k * kSubsetThreads;
+        v[k] = 0;
+        if (j >= 0) {
+          const uint32_t cur = (j <= hi_old) ? src[j] : 0u;
+          const int64_t js = j - qw;
+          const uint32_t hi = (js >= 0 && js <= hi_old) ? src[js] : 0u;
+          const uint32_t lo = (js >= 1 && js - 1 <= hi_old) ? src[js - 1] : 0u;
+          v[k] = cur | __funnelshift_l(lo, hi, r);
+          if (j == words - 1) v[k] &= last_mask;
+        }
       }
       if (kSmem) __syncthreads();  // all loads of this chunk precede its in-place stores
-      if (j >= 0) {
-        if (kSmem) smem_row[j] = v;
-        if (store_global) gdst[j] = v;
+#pragma unroll
+      for (int k = 0; k < kWordsPerThread; ++k) {
+        const int64_t j = top - tid - (int64_t)k * kSubsetThreads;
+        if (j >= 0) {
+          if (kSmem) smem_row[j] = v[k];
+          if (store_global) gdst[j] = v[k];
+        }
       }
     }
     __syncthreads();
