@@ -225,7 +225,7 @@ def compute_only_step_ms(model, batch, loss_fn, steps, warmup, world, dist, devi
     s = torch.cuda.Stream(device)
 
     def step():
-        opt.zero_grad(set_to_none=False)
+        opt.zero_grad(set_to_none=True)
         with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False,
                             enabled=next(model.parameters()).dtype == torch.float32):
             loss = loss_fn(model, batch)

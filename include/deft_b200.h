@@ -156,6 +156,16 @@ deft_status_t deft_sgd_momentum_update_multi(const void* d_grad, int32_t grad_dt
                                              const float* grad_scales, float lr,
                                              float momentum, void* stream);
 
+/* Gather `count` device byte ranges (d_srcs[i], byte_lens[i]) into
+ * d_dst + dst_offsets[i]: the per-parameter gradients autograd just produced
+ * land in their bucket's contiguous slot range in one launch (the store half
+ * of scheduler.py:223-233's store-or-merge; merges accumulate in place).
+ * d_srcs / dst_offsets / byte_lens are HOST arrays (copied into the kernel
+ * parameters, so CUDA-graph captures keep them). */
+deft_status_t deft_gather_segments(void* d_dst, const void* const* d_srcs,
+                                   const int64_t* dst_offsets, const int64_t* byte_lens,
+                                   int32_t count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

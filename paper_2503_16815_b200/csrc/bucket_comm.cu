@@ -540,3 +540,67 @@ cudaError_t launch_sgd_local(const void* grad, int dtype, void* param, float* ma
 }
 
 }  // namespace deft
+
+namespace deft {
+
+// ============================================================================
+// Bucket gather: copy the freshly produced per-parameter gradient tensors of
+// one bucket into its contiguous range of the group slot (one launch per
+// bucket instead of one accumulate kernel per parameter).  The segment table
+// travels in the kernel parameters, so a captured CUDA graph keeps it.
+// ============================================================================
+constexpr int kMaxGatherSeg = 256;
+struct GatherTable {
+  const char* src[kMaxGatherSeg];
+  int64_t dst_off[kMaxGatherSeg];  // bytes from the destination base
+  int64_t first[kMaxGatherSeg + 1];  // prefix of 16-byte units per segment
+  int64_t len[kMaxGatherSeg];      // bytes
+  int32_t count;
+};
+
+__global__ void __launch_bounds__(kLocalThreads) gather_kernel(char* __restrict__ dst,
+                                                              GatherTable t, int64_t total_units) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int seg = 0;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < total_units; u += stride) {
+    while (u >= t.first[seg + 1]) ++seg;
+    const int64_t k = u - t.first[seg];
+    const char* s = t.src[seg] + k * 16;
+    char* d = dst + t.dst_off[seg] + k * 16;
+    const int64_t left = t.len[seg] - k * 16;
+    if (left >= 16 && ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0) {
+      *reinterpret_cast<uint4*>(d) = __ldg(reinterpret_cast<const uint4*>(s));
+    } else {
+      const int64_t n = left < 16 ? left : 16;
+      for (int64_t b = 0; b < n; ++b) d[b] = s[b];
+    }
+  }
+}
+
+}  // namespace deft
+
+namespace deft {
+cudaError_t launch_gather(char* dst, const void* const* srcs, const int64_t* dst_off,
+                          const int64_t* lens, int32_t count, cudaStream_t stream) {
+  for (int32_t s0 = 0; s0 < count; s0 += kMaxGatherSeg) {
+    GatherTable t;
+    t.count = count - s0 < kMaxGatherSeg ? count - s0 : kMaxGatherSeg;
+    t.first[0] = 0;
+    for (int k = 0; k < t.count; ++k) {
+      t.src[k] = reinterpret_cast<const char*>(srcs[s0 + k]);
+      t.dst_off[k] = dst_off[s0 + k];
+      t.len[k] = lens[s0 + k];
+      t.first[k + 1] = t.first[k] + (lens[s0 + k] + 15) / 16;
+    }
+    const int64_t total = t.first[t.count];
+    if (total == 0) continue;
+    int64_t grid = (total + kLocalThreads - 1) / kLocalThreads;
+    if (grid > 148 * 8) grid = 148 * 8;
+    gather_kernel<<<(int)grid, kLocalThreads, 0, stream>>>(dst, t, total);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+}  // namespace deft

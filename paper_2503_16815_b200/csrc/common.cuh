@@ -84,4 +84,7 @@ cudaError_t launch_sgd_local(const void* grad, int dtype, void* param, float* ma
                              const float* scales, float lr, float momentum,
                              cudaStream_t stream);
 
+cudaError_t launch_gather(char* dst, const void* const* srcs, const int64_t* dst_off,
+                          const int64_t* lens, int32_t count, cudaStream_t stream);
+
 }  // namespace deft

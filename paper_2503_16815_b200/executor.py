@@ -319,9 +319,12 @@ class DeftDataParallel:
         owner = self._owner_map([(b.lo, b.hi) for b in self.buckets])
         self._param_buckets = [owner[id(p)] for p in self.params]
         self._bucket_nparams = [0] * len(self.buckets)
-        for bl in self._param_buckets:
+        self._bucket_params: list[list[int]] = [[] for _ in self.buckets]
+        for i, bl in enumerate(self._param_buckets):
             for b in bl:
                 self._bucket_nparams[b] += 1
+                self._bucket_params[b].append(i)
+        self._gather_slot = None
         self.scheduler = DeftScheduler(part, cluster, mult)
         self.capacity_multiplier = mult
         self.planner = ExecutionPlanner(self.scheduler, self.cfg.n_slots, self.cfg.lookahead)
@@ -440,7 +443,32 @@ class DeftDataParallel:
             if self._pending[b] == 0:
                 self._bucket_ready(b)
 
+    def _gather_bucket(self, bidx: int, slot: int):
+        """Copy the bucket's fresh per-parameter gradients into its slot range."""
+        b = self.buckets[bidx]
+        esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
+        srcs, offs, lens = [], [], []
+        for i in self._bucket_params[bidx]:
+            p, o = self.params[i], self.offsets[i]
+            lo, hi = max(b.lo, o), min(b.hi, o + p.numel())
+            g = p.grad
+            if g is None or g.stride() != p.stride() or g.dtype != p.dtype:
+                view = self.comm.grads[slot][lo:hi]
+                if g is None:
+                    view.zero_()
+                else:
+                    self._grad_views[slot][i].copy_(g)
+                continue
+            srcs.append(g.data_ptr() + (lo - o) * esz)
+            offs.append(lo * esz)
+            lens.append((hi - lo) * esz)
+        if srcs:
+            stream = torch.cuda.current_stream(self.device)
+            self.comm.gather(slot, srcs, offs, lens, stream)
+
     def _bucket_ready(self, bidx: int):
+        if self._gather_slot is not None:
+            self._gather_bucket(bidx, self._gather_slot)
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))
         for link, slot in self._fresh_now.pop(bidx, ()):
@@ -464,10 +492,18 @@ class DeftDataParallel:
         with self._autocast():
             loss = loss_fn(self.module, batch)
         if it.zero:
+            # store: autograd allocates fresh gradients (no accumulate kernels) and
+            # each bucket is gathered into the group slot when its backward ends
             if not self._sequential and self._slot_free[it.slot] is not None:
                 comp.wait_event(self._slot_free[it.slot])
-            self.comm.grads[it.slot].zero_()
-        self._bind_grads(it.slot)
+            for p in self.params:
+                p.grad = None
+            self._bound_slot = None
+            self._gather_slot = it.slot
+        else:
+            # merge: accumulate straight into the live group's slot
+            self._bind_grads(it.slot)
+            self._gather_slot = None
         ev_bwd = torch.cuda.Event()
         ev_bwd.record(comp)
         for link, slot, bidx in it.bwd:
