@@ -54,7 +54,7 @@ class DeftConfig:
     momentum: float = 0.9
     partition: PartitionConfig = field(default_factory=PartitionConfig)
     grad_dtype: torch.dtype = torch.float32
-    n_slots: int = 5
+    n_slots: int = 6
     autocast_dtype: torch.dtype | None = torch.bfloat16
     walk: WalkParams | None = None          # run the feedback loop when given
     capacity_multiplier: float = 1.0
@@ -64,7 +64,9 @@ class DeftConfig:
     cuda_graphs: bool = True                # capture + replay each distinct iteration shape
     # where the delayed update of bucket b runs inside its no-read window:
     # "bucket" = right after b's backward (overlaps the rest of the backward),
-    # "end" = after the whole backward (one launch per event at W == 1)
+    # "end" = after the whole backward (one launch per event at W == 1),
+    # "start" = at the start of the iteration it becomes visible in, input-side
+    #           bucket first, each bucket's forward waiting only for its own update
     update_placement: str = "end"
     graph_warmup: int = 1                   # eager runs of a shape before it is captured
 
@@ -327,7 +329,8 @@ class DeftDataParallel:
         self._gather_slot = None
         self.scheduler = DeftScheduler(part, cluster, mult)
         self.capacity_multiplier = mult
-        self.planner = ExecutionPlanner(self.scheduler, self.cfg.n_slots, self.cfg.lookahead)
+        self.planner = ExecutionPlanner(self.scheduler, self.cfg.n_slots, self.cfg.lookahead,
+                                        lag=2 if self.cfg.update_placement == "start" else 1)
         self.link_streams = [torch.cuda.Stream(self.device) for _ in cluster.links]
         # runtime state
         self._slot_free = [None] * self.cfg.n_slots   # event: slot reusable (async mode)
@@ -345,6 +348,9 @@ class DeftDataParallel:
         self._replayed_native = 0
         self._hooks = [p.register_post_accumulate_grad_hook(self._on_grad)
                        for p in self.params]
+        self._fwd_wait = {}
+        if self.cfg.update_placement == "start":
+            self._install_forward_waits()
         return part
 
     def decisions(self, t: int) -> tuple[ScheduleDecision, ScheduleDecision]:
@@ -414,6 +420,44 @@ class DeftDataParallel:
                     lambda: self.comm.update(slot, b.lo, b.hi - b.lo, self.cfg.lr,
                                              self.cfg.momentum, 1.0 / (self.world * k),
                                              self.mom, s), nbytes)
+
+    def _install_forward_waits(self):
+        """"start" placement: the forward pre-hook of every module that owns
+        parameters makes the compute stream wait for the update of the buckets
+        those parameters live in (only the first wait per bucket does anything)."""
+        owner = {id(p): bl for p, bl in zip(self.params, self._param_buckets)}
+        self._fwd_wait: dict[int, torch.cuda.Event] = {}
+
+        def pre(mod, _args):
+            if not self._fwd_wait:
+                return
+            stream = torch.cuda.current_stream(self.device)
+            for b in self._module_buckets[mod]:
+                ev = self._fwd_wait.pop(b, None)
+                if ev is not None:
+                    stream.wait_event(ev)
+
+        self._module_buckets = {}
+        for m in self.module.modules():
+            bl = sorted({b for p in m.parameters(recurse=False) if id(p) in owner
+                         for b in owner[id(p)]})
+            if bl:
+                self._module_buckets[m] = bl
+                self._hooks.append(m.register_forward_pre_hook(pre))
+
+    def _updates_at_start(self, comp, due):
+        """Updates of decision (t-2, backward) at the start of iteration t, input-side
+        bucket first, overlapping the forward: bucket b's forward waits only for b."""
+        ev0 = torch.cuda.Event()
+        ev0.record(comp)
+        s = self.update_stream
+        self._fwd_wait = {}
+        for bidx in range(len(self.buckets) - 1, -1, -1):   # forward order: bucket n first
+            for slot, k in due:
+                self._issue_update(slot, k, bidx, ev0)
+            ev = torch.cuda.Event()
+            ev.record(s)
+            self._fwd_wait[bidx] = ev
 
     def _updates_at_end(self, comp):
         """All due updates after the whole backward (every no-read window is open):
@@ -485,12 +529,18 @@ class DeftDataParallel:
         self._touched = {}      # side streams forked from `comp` in this iteration
         if not self._sequential and self._version_ready is not None:
             comp.wait_event(self._version_ready)   # theta^(t) complete
+        if self.cfg.update_placement == "start" and it.due:
+            self._updates_at_start(comp, it.due)
         ev_fwd = torch.cuda.Event()
         ev_fwd.record(comp)
         for link, slot, bidx in it.fwd:
             self._issue_rs(link, slot, bidx, ev_fwd)
         with self._autocast():
             loss = loss_fn(self.module, batch)
+        if self.cfg.update_placement == "start":
+            for ev in self._fwd_wait.values():   # buckets no forward module touched
+                comp.wait_event(ev)
+            self._fwd_wait = {}
         if it.zero:
             # store: autograd allocates fresh gradients (no accumulate kernels) and
             # each bucket is gathered into the group slot when its backward ends
@@ -509,7 +559,7 @@ class DeftDataParallel:
         for link, slot, bidx in it.bwd:
             self._issue_rs(link, slot, bidx, ev_bwd)
         self._fresh_now = dict(it.fresh)
-        self._due_now = it.due
+        self._due_now = it.due if self.cfg.update_placement != "start" else ()
         self._pending = list(self._bucket_nparams)
         self._fired = [False] * len(self.buckets)
         self._in_step = True

@@ -31,16 +31,25 @@ class IterPlan:
 
 
 class ExecutionPlanner:
-    def __init__(self, scheduler: DeftScheduler, n_slots: int, lookahead: int = 32):
+    """``lag`` = how many iterations after its decision an update event is applied:
+    1 -> during the next backward ("end"/"bucket" placement), 2 -> at the start of
+    the iteration it becomes visible in ("start" placement).  Either way the update
+    of decision (t, backward) is visible from iteration t+2."""
+
+    def __init__(self, scheduler: DeftScheduler, n_slots: int, lookahead: int = 32,
+                 lag: int = 1):
+        if lag not in (1, 2):
+            raise InternalInvariantError("update lag must be 1 or 2")
         self.scheduler = scheduler
         self.n_slots = n_slots
         self.lookahead = lookahead
+        self.lag = lag
+        self._event_queue: list[list[tuple[int, int]]] = []
         self._decisions: dict[int, tuple[ScheduleDecision, ScheduleDecision]] = {}
         self._next = 0
         self.decision_log: list[tuple[ScheduleDecision, ScheduleDecision]] = []
         self._slot_of: dict[int, int] = {}
         self._busy = [False] * n_slots
-        self._due_groups: list[tuple[int, int]] = []
 
     def decisions(self, t: int) -> tuple[ScheduleDecision, ScheduleDecision]:
         while self._next <= t + self.lookahead:
@@ -90,14 +99,15 @@ class ExecutionPlanner:
                     fresh[tr.bucket_id - 1].append((tr.link, slot))
                 else:
                     bwd.append((tr.link, slot, tr.bucket_id - 1))
-        # groups reported by decision (t-1, backward) are updated in this backward
-        due = tuple((self._slot_of[u], k) for u, k in self._due_groups)
+        # groups reported by decision (t-lag, backward) are updated in this iteration
+        due_groups = self._event_queue.pop(0) if len(self._event_queue) >= self.lag else []
+        due = tuple((self._slot_of[u], k) for u, k in due_groups)
         freed = []
-        for u, _ in self._due_groups:
+        for u, _ in due_groups:
             s = self._slot_of.pop(u)
             self._busy[s] = False
             freed.append(s)
-        self._due_groups = [(u, k) for u, k, _ in dB.exec.updates]
+        self._event_queue.append([(u, k) for u, k, _ in dB.exec.updates])
         fresh_t = tuple(sorted((b, tuple(v)) for b, v in fresh.items()))
         key = (fwd, slot, new, tuple(bwd), fresh_t, due)
         return IterPlan(t, slot, new, fwd, tuple(bwd), fresh_t, due, tuple(freed), key)

@@ -50,7 +50,7 @@ def uniform_buckets(n, comm_us=900, fwd_total=3600, bwd_total=7200):
 
 
 def spec_inputs(entry, inputs):
-    """(raw profile dict, cluster dict, partition cfg or None, bw, mult, iterations)."""
+    """(raw profile dict, cluster dict, partition cfg or None, comm factor, mult, iterations)."""
     spec = entry["spec"]
     if "uniform" in spec:
         prof = {"name": f"uniform{spec['uniform']}", "batch_size": 256, "learning_rate": 0.01,
@@ -61,4 +61,7 @@ def spec_inputs(entry, inputs):
     mult = 1.0
     for _ in range(spec.get("mult_steps", 0)):
         mult *= 1.1
-    return prof, cluster, spec.get("partition"), spec.get("bw_scale", 1.0), mult, entry["iterations"]
+    # comm factor applied with ModelProfile.scaled_comm (profiles.py:134-152):
+    # 1/bw_scale for the reference's bandwidth sweep points, or an explicit comm_scale
+    factor = spec["comm_scale"] if "comm_scale" in spec else 1.0 / spec.get("bw_scale", 1.0)
+    return prof, cluster, spec.get("partition"), factor, mult, entry["iterations"]

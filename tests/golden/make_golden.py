@@ -300,6 +300,37 @@ def main():
                                "partition": {"partition_size": 6_500_000, "mu": mu_of[cname]},
                                "iterations": 12}})
 
+    # profiles MEASURED on B200s by bench.py --dump-profile (the
+    # profiler's JSON is also the input to reference parity).  NVLink comm is tiny
+    # next to compute, so comm is also scaled up to drive the merge regimes.
+    prof_dir = OUT.parent.parent / "profiles"
+    for path in sorted(prof_dir.glob("r01_measured_profile_*.json")):
+        doc = json.loads(path.read_text())
+        mprof = ds.profile_from_dict(doc["profile"])
+        mcl = ds.cluster_from_dict(doc["cluster"])
+        tag = path.stem.replace("r01_measured_profile_", "measured_")
+        inputs["profiles"][tag] = doc["profile"]
+        inputs["clusters"][tag] = doc["cluster"]
+        mu = max(l.speed_ratio_to_fast for l in mcl.links)
+        for scale in (1.0, 60.0, 200.0):
+            p = mprof if scale == 1.0 else mprof.scaled_comm(scale)
+            cfg = ds.PartitionConfig(partition_size=6_500_000, mu=mu)
+            key = f"{tag}__x{int(scale)}"
+            s = ds.deft_schedule(p, mcl, cfg, 100)
+            final, v = ds.feedback_loop(p, mcl, cfg, walk, iterations=100)
+            final_lines = [json.dumps(d.to_dict(), sort_keys=True) for d in final.decisions]
+            verdict = {"preserved": v.preserved, "ratio": v.ratio,
+                       "expected_state": v.expected_state, "baseline_state": v.baseline_state,
+                       "k_values": list(v.sequence.k_values), "retries": v.retries,
+                       "capacity_multiplier": v.capacity_multiplier,
+                       "final_sha256": hashlib.sha256(
+                           ("\n".join(final_lines) + "\n").encode()).hexdigest()}
+            add_schedule(key, s, verdict,
+                         {"spec": {"profile": tag, "cluster": tag, "comm_scale": scale,
+                                   "partition": {"partition_size": 6_500_000, "mu": mu},
+                                   "iterations": 100}})
+    (OUT / "inputs.json").write_text(json.dumps(inputs, indent=1, sort_keys=True))
+
     (OUT / "partition.json").write_text(json.dumps(part_rows, indent=0, sort_keys=True))
     (OUT / "schedules.json").write_text(json.dumps(index, indent=0, sort_keys=True))
 

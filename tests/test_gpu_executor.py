@@ -17,22 +17,25 @@ def need_gpu():
         pytest.skip("no CUDA device")
 
 
+@pytest.mark.parametrize("placement", ["end", "bucket", "start"])
 @pytest.mark.parametrize("graphs", [True, False])
 @pytest.mark.parametrize("iterations,comm_us", [(12, 900), (25, 900), (20, 300), (16, 1900)])
-def test_single_gpu_matches_oracle(iterations, comm_us, graphs):
+def test_single_gpu_matches_oracle(iterations, comm_us, graphs, placement):
     theta, theta0, decisions = S.run_executor(1, 0, iterations, comm_us=comm_us,
-                                              cuda_graphs=graphs)
+                                              cuda_graphs=graphs, placement=placement)
     want = S.oracle_theta(theta0, decisions, 1, iterations)
     assert S.rel_err(theta, want) <= S.TOL
 
 
+@pytest.mark.parametrize("placement", ["end", "start"])
 @pytest.mark.parametrize("graphs", [True, False])
-def test_bf16_params_single_gpu(graphs):
+def test_bf16_params_single_gpu(graphs, placement):
     """bf16 model (bf16 grads, as the GPT-2 config): the fp32 master follows the
     oracle within 1e-6 and the bf16 parameters are its round-to-nearest copy."""
     iters = 16
     theta, theta0, decisions, params = S.run_executor(
-        1, 0, iters, dtype=torch.bfloat16, cuda_graphs=graphs, grad_fn=S.flat_grad_dyadic)
+        1, 0, iters, dtype=torch.bfloat16, cuda_graphs=graphs, grad_fn=S.flat_grad_dyadic,
+        placement=placement)
     assert max(u["merge_count"] for d in decisions for u in d["update_events"]) >= 2
     want = S.oracle_theta(theta0, decisions, 1, iters, grad_fn=S.flat_grad_dyadic)
     assert S.rel_err(theta, want) <= S.TOL
@@ -47,7 +50,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, iterations, comm_us, graphs, q, bf16=False):
+def _worker(rank, world, port, iterations, comm_us, graphs, q, bf16=False, placement="end"):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
@@ -57,20 +60,21 @@ def _worker(rank, world, port, iterations, comm_us, graphs, q, bf16=False):
         if bf16:
             theta, theta0, decisions, params = S.run_executor(
                 world, rank, iterations, comm_us=comm_us, cuda_graphs=graphs,
-                dtype=torch.bfloat16, grad_fn=S.flat_grad_dyadic)
+                dtype=torch.bfloat16, grad_fn=S.flat_grad_dyadic, placement=placement)
             q.put((rank, theta, theta0, decisions, params))
         else:
             theta, theta0, decisions = S.run_executor(world, rank, iterations, comm_us=comm_us,
-                                                      cuda_graphs=graphs)
+                                                      cuda_graphs=graphs, placement=placement)
             q.put((rank, theta, theta0, decisions))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.multigpu
-@pytest.mark.parametrize("graphs", [True, False])
+@pytest.mark.parametrize("graphs,placement", [(True, "end"), (False, "end"), (True, "start"),
+                                              (False, "bucket")])
 @pytest.mark.parametrize("iterations,comm_us", [(14, 900), (20, 1900)])
-def test_multi_gpu_matches_oracle(iterations, comm_us, graphs):
+def test_multi_gpu_matches_oracle(iterations, comm_us, graphs, placement):
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -78,7 +82,8 @@ def test_multi_gpu_matches_oracle(iterations, comm_us, graphs):
     ctx = torch.multiprocessing.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, iterations, comm_us, graphs, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, iterations, comm_us, graphs, q, False,
+                                             placement))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -112,7 +117,8 @@ def shard_range(offset, numel, r, world, align):
 
 
 @pytest.mark.multigpu
-def test_multi_gpu_bf16_matches_oracle():
+@pytest.mark.parametrize("placement", ["end", "start"])
+def test_multi_gpu_bf16_matches_oracle(placement):
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -120,7 +126,8 @@ def test_multi_gpu_bf16_matches_oracle():
     ctx = torch.multiprocessing.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, iterations, 900, True, q, True))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, iterations, 900, True, q, True,
+                                               placement))
              for r in range(world)]
     for p in procs:
         p.start()

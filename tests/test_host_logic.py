@@ -20,10 +20,10 @@ def oracle_dp():
 
 
 def build_product_inputs(entry, inputs):
-    prof_d, cluster_d, part, bw, mult, iters = spec_inputs(entry, inputs)
+    prof_d, cluster_d, part, factor, mult, iters = spec_inputs(entry, inputs)
     prof = D.profile_from_dict(prof_d)
-    if bw != 1.0:
-        prof = prof.scaled_comm(1.0 / bw)
+    if factor != 1.0:
+        prof = prof.scaled_comm(factor)
     cluster = D.cluster_from_dict(cluster_d)
     cfg = D.PartitionConfig(**part) if part else None
     return prof, cluster, cfg, mult, iters

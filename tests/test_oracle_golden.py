@@ -61,10 +61,10 @@ def test_partition_matches_reference(golden_inputs):
 
 
 def _oracle_stream(entry, inputs):
-    prof, cluster, part, bw, mult, iters = spec_inputs(entry, inputs)
+    prof, cluster, part, factor, mult, iters = spec_inputs(entry, inputs)
     buckets = prof["buckets"]
-    if bw != 1.0:
-        buckets = O.scaled_comm(buckets, 1.0 / bw)
+    if factor != 1.0:
+        buckets = O.scaled_comm(buckets, factor)
     if part is not None:
         buckets = O.partition(buckets, sum(b["forward_us"] for b in buckets),
                               part["partition_size"], part["mu"])

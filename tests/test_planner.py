@@ -17,49 +17,43 @@ from paper_2503_16815_b200.planner import ExecutionPlanner
 from test_host_logic import build_product_inputs
 
 
-def _planner_for(entry, inputs, n_slots=5):
+def _planner_for(entry, inputs, n_slots=6, lag=1):
     prof, cluster, cfg, mult, iters = build_product_inputs(entry, inputs)
     part = D.partition_buckets(prof, cfg) if cfg is not None else prof
-    return ExecutionPlanner(D.DeftScheduler(part, cluster, mult), n_slots), part, iters
+    return ExecutionPlanner(D.DeftScheduler(part, cluster, mult), n_slots, lag=lag), part, iters
 
 
 def check_invariants(planner, n_buckets, iters):
-    live = {}            # slot -> set of bucket indices still to transfer for its group
-    pending_update = {}  # slot -> merge_count, group fully sent, update next iteration
+    """Slots: a store never reuses a live slot; every transfer reads a live slot
+    still owing that bucket; a group is updated exactly `lag` iterations after
+    the decision reporting it, once all its buckets were sent; <= n_slots live."""
+    live = {}        # slot -> set of bucket indices still to transfer
+    reported = {}    # slot -> (iteration of the reporting decision, merge_count)
     for t in range(iters):
         p = planner.plan(t)
-        # updates due now: groups reported last iteration, all buckets sent
         for slot, k in p.due:
-            assert slot in pending_update and pending_update.pop(slot) == k
+            it, kk = reported.pop(slot)
+            assert (it, kk) == (t - planner.lag, k), (t, slot)
+            del live[slot]
+        assert sorted(p.freed) == sorted(s for s, _ in p.due)
         for link, slot, b in p.fwd + p.bwd:
             assert slot in live and b in live[slot], (t, slot, b)
             live[slot].discard(b)
         if p.zero:
-            assert p.slot not in live and p.slot not in pending_update, "slot reused while live"
+            assert p.slot not in live, "slot reused while live"
             live[p.slot] = set(range(n_buckets))
         else:
-            assert p.slot in live
+            assert p.slot in live and p.slot not in reported
         for b, pairs in p.fresh:
             for link, slot in pairs:
                 assert slot == p.slot and b in live[slot]
                 live[slot].discard(b)
         d_b = planner.decision_log[t][1]
-        for uid, k, _ in d_b.exec.updates:
-            # the group's slot is fully sent when its event is reported
-            emptied = [s for s, left in live.items() if not left and s not in pending_update]
-            assert emptied, (t, uid)
-        for s in [s for s, left in live.items() if not left]:
-            pending_update[s] = None
-        for s in list(pending_update):
-            if pending_update[s] is None:
-                del live[s]
-        # attach merge counts to the groups reported in this decision
-        reported = [k for _, k, _ in d_b.exec.updates]
-        empty_slots = [s for s, v in pending_update.items() if v is None]
-        assert len(empty_slots) == len(reported), (t, empty_slots, reported)
-        for s, k in zip(sorted(empty_slots, key=lambda s: -1), reported):
-            pending_update[s] = k
-        assert len(live) + len(pending_update) <= planner.n_slots
+        done = sorted(s for s, left in live.items() if not left and s not in reported)
+        assert len(done) == len(d_b.exec.updates), (t, done, d_b.exec.updates)
+        for (uid, k, _), s_ in zip(d_b.exec.updates, done):
+            reported[s_] = (t, k)
+        assert len(live) <= planner.n_slots
 
 
 @pytest.fixture(autouse=True)
@@ -68,12 +62,13 @@ def oracle_dp():
         yield
 
 
-def test_planner_invariants_on_golden_streams(golden_index, golden_inputs):
+@pytest.mark.parametrize("lag", [1, 2])
+def test_planner_invariants_on_golden_streams(golden_index, golden_inputs, lag):
     checked = 0
     for e in golden_index:
         if len(e["partitioned"]) > 60:
             continue
-        planner, part, iters = _planner_for(e, golden_inputs)
+        planner, part, iters = _planner_for(e, golden_inputs, lag=lag)
         check_invariants(planner, part.n_buckets, min(iters, 120))
         checked += 1
     assert checked >= 45
