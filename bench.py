@@ -44,7 +44,7 @@ def parse():
                          "NCCL WFBP baseline)")
     ap.add_argument("--batch", type=int, default=None,
                     help="per-GPU batch (default 64; GPT-2: 16 sequences of 1024)")
-    ap.add_argument("--update-placement", default="end", choices=["bucket", "end"])
+    ap.add_argument("--update-placement", default="end", choices=["bucket", "end", "start"])
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs")
     ap.add_argument("--bucket-mb", type=float, default=None,
                     help="partition size in MB of fp32 (default: the reference's 6.5M params)")

@@ -652,8 +652,24 @@ class DeftDataParallel:
         return loss
 
     def finish(self):
-        """Drain every stream (the trailing in-flight groups stay unapplied, as
-        in the reference where unaccounted iterations are still in flight)."""
+        """Make theta^(t) current (t = iterations run) and drain every stream.
+        With "start" placement the updates that become visible at iteration t are
+        applied here (they would otherwise run at the start of iteration t); groups
+        still in flight stay unapplied, as in the reference where unaccounted
+        iterations are still in flight."""
+        if self.cfg.update_placement == "start" and hasattr(self, "planner"):
+            due, freed = self.planner.take_pending()
+            if due:
+                caller = torch.cuda.current_stream(self.device)
+                self.compute_stream.wait_stream(caller)
+                with torch.cuda.stream(self.compute_stream):
+                    comp = self.compute_stream
+                    self._touched = {}
+                    self._updates_at_start(comp, due)
+                    for ev in self._fwd_wait.values():
+                        comp.wait_event(ev)
+                    self._fwd_wait = {}
+                caller.wait_stream(self.compute_stream)
         torch.cuda.synchronize(self.device)
 
     def timing_summary(self) -> dict:

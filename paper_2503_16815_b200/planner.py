@@ -73,6 +73,22 @@ class ExecutionPlanner:
         raise InternalInvariantError(
             f"all {self.n_slots} gradient slots are held by live groups; raise n_slots")
 
+    def take_pending(self) -> tuple[tuple, tuple]:
+        """("start" placement) updates that are due at the start of the NEXT
+        iteration, handed out early so a caller can make theta^(t) current
+        without running iteration t.  Returns (due, freed)."""
+        if self.lag != 2 or len(self._event_queue) < self.lag:
+            return (), ()
+        due_groups = self._event_queue.pop(0)
+        due = tuple((self._slot_of[u], k) for u, k in due_groups)
+        freed = []
+        for u, _ in due_groups:
+            s = self._slot_of.pop(u)
+            self._busy[s] = False
+            freed.append(s)
+        self._event_queue.insert(0, [])   # keep the queue's timing for the next plan()
+        return due, tuple(freed)
+
     def plan(self, t: int) -> IterPlan:
         if t != len(self.decision_log):
             raise InternalInvariantError("iterations must be planned in order")

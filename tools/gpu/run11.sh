@@ -1,5 +1,5 @@
 # full GPU suite (2 GPUs), smoke, placement comparison at N=1 and N=2
-timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
+timeout 900 python -m pytest tests -q -m gpu 2>&1 | tail -12
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
 for PL in end start; do
 CUDA_VISIBLE_DEVICES=0 timeout 600 python bench.py --no-cpu-baseline --update-placement $PL > gpurun_out/b11_n1_$PL.json 2> gpurun_out/b11_n1_$PL.err; echo "n1 $PL rc=$?"
