@@ -292,8 +292,7 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
             t = torch.tensor([ms], device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        n = 1 if (kind == "update" and world == 1 and ddp.cfg.update_placement == "end") \
-            else len(ddp.buckets)
+        n = 1 if (kind == "update" and ddp.cfg.update_placement == "end") else len(ddp.buckets)
         out[kind] = {"launches": n, "ms_per_pass": round(ms, 4),
                      "avg_launch_us": round(ms / n * 1e3, 2), "bytes_per_pass": nbytes,
                      "achieved_gbs": round(nbytes / (ms / 1e3) / 1e9, 1)}
@@ -308,9 +307,9 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
         upd_bytes = sum((b.hi - b.lo) * esz * (world - 1) // world for b in ddp.buckets)
 
     def updates():
-        if world == 1 and ddp.cfg.update_placement == "end":   # the step's own launch shape
-            ddp.comm.update_local_multi(slot, [(b.lo, b.hi) for b in ddp.buckets], 1.0, 0.0,
-                                        0.9, ddp.mom, s)
+        if ddp.cfg.update_placement == "end":   # the step's own launch shape
+            ddp.comm.update_multi(slot, [(b.lo, b.hi) for b in ddp.buckets], 1.0, 0.0, 0.9,
+                                  ddp.mom, s)
             return
         for b in ddp.buckets:
             ddp.comm.update(slot, b.lo, b.hi - b.lo, 0.0, 0.9, 1.0, ddp.mom, s)
@@ -463,8 +462,7 @@ def main():
             ms = float(t.item())
         return ms
 
-    for _ in range(args.warmup):
-        ddp.train_step(batch, loss_fn)
+    warm = ddp.warm_up(batch, loss_fn, min_steps=args.warmup)  # until steady-state replay
     if ddp.static_batch is not None:
         batch = ddp.static_batch      # graphs read these; no per-step device copy
     n0 = ddp.native_launches()
@@ -533,7 +531,10 @@ def main():
         avg_ms = r["ms"] / r["launches"]
         in_step = (r["bytes"] / r["launches"]) / (avg_ms / 1e3) / 1e9
     achieved = iso[kind]["achieved_gbs"]
-    roof = {"kernel": {"update": "sgd_local_kernel" if world == 1 else "update_allgather_kernel",
+    upd_name = "sgd_local_kernel" if world == 1 else (
+        "update_allgather_multi_kernel" if ddp.cfg.update_placement == "end"
+        else "update_allgather_kernel")
+    roof = {"kernel": {"update": upd_name,
                        "reduce_scatter": "reduce_scatter_kernel"}[kind],
             "bound": "hbm" if hbm_bound else "nvlink",
             "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -576,7 +577,8 @@ def main():
                        "partition_size": psize, "comm_scale": args.comm_scale,
                        "merge_counts": sorted({u.merge_count for pair in ddp.decision_log
                                                for d in pair for u in d.update_events}),
-                       "cuda_graphs": ddp.cfg.cuda_graphs, "setup_s": round(t_setup, 2)},
+                       "cuda_graphs": ddp.cfg.cuda_graphs, "graphs_captured": len(ddp._graphs),
+                       "warmup_steps_run": warm, "setup_s": round(t_setup, 2)},
             "e2e": {"value": round(e2e_value, 2), "unit": "samples/s",
                     "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": 4,
                     "note": "H2D on a copy stream, double-buffered (copy of step t+1 "

@@ -140,6 +140,14 @@ deft_status_t deft_bucket_update(deft_comm* c, int32_t slot, int64_t offset, int
                                  float lr, float momentum, float grad_scale, float* d_mom,
                                  void* stream);
 
+/* Every bucket of one update event ([offsets[k], offsets[k]+numels[k]) of slot
+ * `slot`, host arrays) in ONE launch with one entry/exit barrier pair per CTA;
+ * same arithmetic as deft_bucket_update. */
+deft_status_t deft_bucket_update_multi(deft_comm* c, int32_t slot, int32_t count,
+                                       const int64_t* offsets, const int64_t* numels, float lr,
+                                       float momentum, float grad_scale, float* d_mom,
+                                       void* stream);
+
 /* Local (W == 1 or rank-private) fused update over device arrays:
  * v = m*v + s*g ; p -= lr*v. grad_dtype as above; d_param has the grad dtype;
  * for bf16 the fp32 master d_master is updated and rounded into d_param. */

@@ -135,22 +135,16 @@ class BucketComm:
             (ctypes.c_int64 * n)(*byte_lens), n, c_vp(stream.cuda_stream)),
             "deft_gather_segments")
 
-    def update_local_multi(self, slot: int, ranges, scale: float, lr: float, momentum: float,
-                           mom: torch.Tensor, stream) -> None:
-        """W == 1: every bucket of one update event in ONE launch."""
-        if self.world != 1:
-            raise ValueError("update_local_multi is the single-rank path")
+    def update_multi(self, slot: int, ranges, scale: float, lr: float, momentum: float,
+                     mom: torch.Tensor, stream) -> None:
+        """Every bucket of one update event in ONE launch (deft_bucket_update_multi):
+        the local fused update at W == 1, update + parameter all-gather at W > 1."""
         n = len(ranges)
         offs = (ctypes.c_int64 * n)(*[lo for lo, _ in ranges])
         lens = (ctypes.c_int64 * n)(*[hi - lo for lo, hi in ranges])
-        scales = (ctypes.c_float * n)(*([scale] * n))
-        esz = 2 if self.grad_dtype == torch.bfloat16 else 4
-        g = self._g.ptr.value + slot * self.slot_elems * esz
-        master = c_vp(self.master.data_ptr() if self.master is not None else None)
-        check(_native.lib().deft_sgd_momentum_update_multi(
-            c_vp(g), DTYPE_BF16 if self.grad_dtype == torch.bfloat16 else DTYPE_F32,
-            c_vp(self._p.ptr.value), master, c_vp(mom.data_ptr()), n, offs, lens, scales, lr,
-            momentum, c_vp(stream.cuda_stream)), "deft_sgd_momentum_update_multi")
+        check(_native.lib().deft_bucket_update_multi(
+            self._h, slot, n, offs, lens, lr, momentum, scale, c_vp(mom.data_ptr()),
+            c_vp(stream.cuda_stream)), "deft_bucket_update_multi")
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None:

@@ -604,3 +604,118 @@ cudaError_t launch_gather(char* dst, const void* const* srcs, const int64_t* dst
   return cudaSuccess;
 }
 }  // namespace deft
+
+namespace deft {
+
+// ============================================================================
+// Multi-bucket fused update + all-gather (W > 1): every bucket of one update
+// event in ONE launch with ONE entry/exit barrier pair per CTA.  The table
+// holds this rank's owned shard of each bucket (segments over the same flat
+// index space on every rank); the grid is a function of the bucket sizes only,
+// so block b meets block b of every peer.
+// ============================================================================
+template <typename T, int W>
+__global__ void __launch_bounds__(kLocalThreads) update_allgather_multi_kernel(
+    PeerPtrs P, int rank, int64_t slot_base, SegTable t, float lr, float momentum,
+    float* __restrict__ mom) {
+  using V = Vec<T>;
+  constexpr bool kMaster = sizeof(T) == 2;
+  const uint32_t epoch = take_epochs(P, rank, kBarrierUpdate, 2u);
+  peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 1u);
+  const T* g = reinterpret_cast<const T*>(P.grads[rank]) + slot_base;
+  float* ref = kMaster ? P.master : reinterpret_cast<float*>(P.params[rank]);
+  T* dst[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) dst[k] = reinterpret_cast<T*>(P.params[k]);
+  auto one = [&](int64_t e, float s) {
+    const float v = fmaf(momentum, mom[e], V::scalar(g + e) * s);
+    mom[e] = v;
+    const float p = fmaf(-lr, v, ref[e]);
+    if (kMaster) ref[e] = p;
+#pragma unroll
+    for (int k = 0; k < W; ++k) store1(dst[k] + e, p);
+  };
+  const int64_t total = t.first_vec[t.count];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int seg = 0;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < total; u += stride) {
+    while (u >= t.first_vec[seg + 1]) ++seg;
+    const int64_t base = t.off[seg];
+    const int64_t end = base + t.len[seg];
+    const int64_t aligned = (base + 3) / 4 * 4;
+    const int64_t k = u - t.first_vec[seg];
+    const float s = t.scale[seg];
+    if (k == 0 && aligned > base) {
+      for (int64_t e = base; e < aligned && e < end; ++e) one(e, s);
+    }
+    const int64_t e = aligned + k * 4;
+    if (e + 4 <= end) {
+      const float4 g4 = load4(g + e);
+      float4 m4 = load4(mom + e);
+      float4 p4 = load4(ref + e);
+      m4.x = fmaf(momentum, m4.x, g4.x * s);
+      m4.y = fmaf(momentum, m4.y, g4.y * s);
+      m4.z = fmaf(momentum, m4.z, g4.z * s);
+      m4.w = fmaf(momentum, m4.w, g4.w * s);
+      p4.x = fmaf(-lr, m4.x, p4.x);
+      p4.y = fmaf(-lr, m4.y, p4.y);
+      p4.z = fmaf(-lr, m4.z, p4.z);
+      p4.w = fmaf(-lr, m4.w, p4.w);
+      store4(mom + e, m4);
+      if (kMaster) store4(ref + e, p4);
+#pragma unroll
+      for (int kk = 0; kk < W; ++kk) store4(dst[kk] + e, p4);
+    } else {
+      for (int64_t x = e; x < end; ++x) one(x, s);
+    }
+  }
+  peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 2u);
+}
+
+cudaError_t launch_update_allgather_multi(const PeerPtrs& P, int rank, int world, int dtype,
+                                          int64_t slot_base, int32_t count,
+                                          const int64_t* offsets, const int64_t* numels,
+                                          float lr, float momentum, float grad_scale,
+                                          float* mom, cudaStream_t stream) {
+  const int align = dtype == 0 ? 4 : 8;
+  for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
+    SegTable t{};
+    t.count = count - s0 < kMaxSeg ? count - s0 : kMaxSeg;
+    t.first_vec[0] = 0;
+    int64_t total_elems = 0;
+    for (int k = 0; k < t.count; ++k) {
+      const ShardRange sh = shard_of(offsets[s0 + k], numels[s0 + k], rank, world, align);
+      t.off[k] = sh.lo;
+      t.len[k] = sh.hi - sh.lo;
+      t.scale[k] = grad_scale;
+      const int64_t aligned = (sh.lo + 3) / 4 * 4;
+      int64_t units = sh.hi > aligned ? (sh.hi - aligned + 3) / 4 : 0;
+      if (units == 0 && t.len[k] > 0) units = 1;
+      t.first_vec[k + 1] = t.first_vec[k] + units;
+      total_elems += numels[s0 + k];
+    }
+    // identical on every rank: depends on the bucket sizes, not on this rank's shards
+    int grid = comm_grid_for((total_elems + world - 1) / world);
+#define DEFT_UPM_CASE(WW)                                                                   \
+  case WW:                                                                                  \
+    if (dtype == 0)                                                                         \
+      update_allgather_multi_kernel<float, WW><<<grid, kLocalThreads, 0, stream>>>(         \
+          P, rank, slot_base, t, lr, momentum, mom);                                        \
+    else                                                                                    \
+      update_allgather_multi_kernel<__nv_bfloat16, WW><<<grid, kLocalThreads, 0, stream>>>( \
+          P, rank, slot_base, t, lr, momentum, mom);                                        \
+    break;
+    switch (world) {
+      DEFT_UPM_CASE(2) DEFT_UPM_CASE(3) DEFT_UPM_CASE(4) DEFT_UPM_CASE(5)
+      DEFT_UPM_CASE(6) DEFT_UPM_CASE(7) DEFT_UPM_CASE(8)
+      default: break;
+    }
+#undef DEFT_UPM_CASE
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace deft

@@ -485,3 +485,31 @@ extern "C" deft_status_t deft_gather_segments(void* d_dst, const void* const* d_
   if (e != cudaSuccess) return cuda_fail(e, "gather_kernel");
   return DEFT_OK;
 }
+
+extern "C" deft_status_t deft_bucket_update_multi(deft_comm* c, int32_t slot, int32_t count,
+                                                 const int64_t* offsets, const int64_t* numels,
+                                                 float lr, float momentum, float grad_scale,
+                                                 float* d_mom, void* stream) {
+  if (!c) return fail(DEFT_ERR_INVALID_ARGUMENT, "null comm");
+  if (count <= 0) return DEFT_OK;
+  for (int32_t k = 0; k < count; ++k) {
+    deft_status_t st = check_range(c, slot, offsets[k], numels[k]);
+    if (st != DEFT_OK) return st;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t slot_base = (int64_t)slot * c->slot_elems;
+  if (c->world == 1) {
+    const int esz = c->dtype == DEFT_DTYPE_F32 ? 4 : 2;
+    std::vector<float> scales(count, grad_scale);
+    cudaError_t e = launch_sgd_local(c->P.grads[0] + slot_base * esz, c->dtype, c->P.params[0],
+                                     c->P.master, d_mom, count, offsets, numels, scales.data(),
+                                     lr, momentum, s);
+    if (e != cudaSuccess) return cuda_fail(e, "sgd_local_kernel");
+    return DEFT_OK;
+  }
+  cudaError_t e = launch_update_allgather_multi(c->P, c->rank, c->world, c->dtype, slot_base,
+                                                count, offsets, numels, lr, momentum, grad_scale,
+                                                d_mom, s);
+  if (e != cudaSuccess) return cuda_fail(e, "update_allgather_multi_kernel");
+  return DEFT_OK;
+}

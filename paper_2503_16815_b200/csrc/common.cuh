@@ -84,6 +84,11 @@ cudaError_t launch_sgd_local(const void* grad, int dtype, void* param, float* ma
                              const float* scales, float lr, float momentum,
                              cudaStream_t stream);
 
+cudaError_t launch_update_allgather_multi(const PeerPtrs& P, int rank, int world, int dtype,
+                                          int64_t slot_base, int32_t count,
+                                          const int64_t* offsets, const int64_t* numels,
+                                          float lr, float momentum, float grad_scale,
+                                          float* mom, cudaStream_t stream);
 cudaError_t launch_gather(char* dst, const void* const* srcs, const int64_t* dst_off,
                           const int64_t* lens, int32_t count, cudaStream_t stream);
 

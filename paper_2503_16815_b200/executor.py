@@ -346,6 +346,7 @@ class DeftDataParallel:
         self._pool = torch.cuda.graph_pool_handle() if self.cfg.cuda_graphs else None
         self._captured_native = 0
         self._replayed_native = 0
+        self.last_step_kind = None
         self._hooks = [p.register_post_accumulate_grad_hook(self._on_grad)
                        for p in self.params]
         self._fwd_wait = {}
@@ -461,22 +462,18 @@ class DeftDataParallel:
 
     def _updates_at_end(self, comp):
         """All due updates after the whole backward (every no-read window is open):
-        one multi-bucket launch per group on the compute stream at W == 1; per
-        bucket update + all-gather kernels on the update stream at W > 1."""
+        one multi-bucket launch per update event on the compute stream -- the local
+        fused update at W == 1, the fused update + parameter all-gather at W > 1."""
+        ranges = [(b.lo, b.hi) for b in self.buckets]
+        esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
         if self.world == 1:
-            ranges = [(b.lo, b.hi) for b in self.buckets]
-            esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
             nbytes = self.total * 20  # read g, v, p(master); write v, p (+bf16 copy)
-            for slot, k in self._due_now:
-                self._timed("update", comp, lambda: self.comm.update_local_multi(
-                    slot, ranges, 1.0 / k, self.cfg.lr, self.cfg.momentum, self.mom, comp),
-                    nbytes)
-            return
-        ev = torch.cuda.Event()
-        ev.record(comp)
+        else:
+            nbytes = self.total * esz * (self.world - 1) // self.world  # crossing NVLink
         for slot, k in self._due_now:
-            for bidx in range(len(self.buckets)):
-                self._issue_update(slot, k, bidx, ev)
+            self._timed("update", comp, lambda: self.comm.update_multi(
+                slot, ranges, 1.0 / (self.world * k), self.cfg.lr, self.cfg.momentum, self.mom,
+                comp), nbytes)
 
     def _on_grad(self, p):
         if not self._in_step:
@@ -625,8 +622,22 @@ class DeftDataParallel:
         caller.wait_stream(self.compute_stream)
         return loss
 
+    def warm_up(self, batch, loss_fn: Callable, min_steps: int = 3, max_steps: int = 64,
+                steady: int = 6) -> int:
+        """Run steps until the last `steady` were all graph replays (every
+        steady-state iteration shape captured); returns the number of steps run."""
+        streak, n = 0, 0
+        while n < max_steps and (n < min_steps or streak < steady):
+            self.train_step(batch, loss_fn)
+            n += 1
+            streak = streak + 1 if self.last_step_kind == "replay" else 0
+            if not self._sequential:
+                streak = steady
+        return n
+
     def _dispatch(self, it: IterPlan, batch, loss_fn: Callable) -> torch.Tensor:
         if not self._sequential or self.cfg.instrument:
+            self.last_step_kind = "eager"
             return self._run_iteration(it, batch, loss_fn)
         static = self._static_inputs(batch)
         hit = self._graphs.get(it.key)
@@ -634,10 +645,12 @@ class DeftDataParallel:
             g, loss, n = hit
             g.replay()
             self._replayed_native += n
+            self.last_step_kind = "replay"
             return loss
         seen = self._seen.get(it.key, 0)
         self._seen[it.key] = seen + 1
         if seen < self.cfg.graph_warmup:
+            self.last_step_kind = "eager"
             return self._run_iteration(it, static, loss_fn)
         self.compute_stream.synchronize()
         g = torch.cuda.CUDAGraph()
@@ -649,6 +662,7 @@ class DeftDataParallel:
         self._graphs[it.key] = (g, loss, n)
         g.replay()
         self._replayed_native += n
+        self.last_step_kind = "capture"
         return loss
 
     def finish(self):

@@ -34,8 +34,7 @@ def main():
     ddp = D.DeftDataParallel(model, cfg)
     ddp.measure_profile(batch, loss_fn, iters=2, name=args.model, batch_size=64)
     ddp.plan()
-    for _ in range(4):
-        ddp.train_step(batch, loss_fn)
+    ddp.warm_up(batch, loss_fn)
     if ddp.static_batch is not None:
         batch = ddp.static_batch
     torch.cuda.synchronize()
