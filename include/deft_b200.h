@@ -79,6 +79,20 @@ deft_status_t deft_solver_destroy(deft_solver* s);
 deft_status_t deft_solver_solve(deft_solver* s, int32_t batch, const int32_t* n_items,
                                 const int64_t* weights, const int64_t* caps,
                                 uint8_t* take_out, int64_t* best_out);
+/* K5: the DeFT delayed-update state machine (scheduler.py:159-342) for
+ * `instances` independent schedulers over one partitioned profile (n buckets,
+ * ids 1..n; comm / backward times in us) and n_links links, each instance with
+ * its own per-link forward / backward stage capacities (the host computes them
+ * with the reference's float rounding, scheduler.py:121-125), `iterations`
+ * iterations, ONE persistent launch (one CTA per instance).  Writes compact
+ * decision records (layout: csrc/scheduler_kernel.cu) into out[i*out_stride..],
+ * used[i] ints each, and status[i] (0, or -4 = unsupported: scaled-mode
+ * capacities above 1e7 us; -3 = out_stride too small; -6 = invariant). */
+deft_status_t deft_solver_schedule(deft_solver* s, int32_t instances, int32_t n,
+                                   int32_t n_links, int32_t iterations, const int64_t* comm,
+                                   const int64_t* bwd, const int64_t* fwd_caps,
+                                   const int64_t* bwd_caps, int32_t* out, int64_t out_stride,
+                                   int64_t* used, int32_t* status);
 /* Device time (ms) of the kernels of the last solve, measured with CUDA events. */
 float deft_solver_last_kernel_ms(const deft_solver* s);
 

@@ -21,7 +21,7 @@ EXPORTED = (
     "deft_abi_version", "deft_last_error", "deft_launch_count",
     "deft_subset_sum_workspace_bytes", "deft_subset_sum_batched",
     "deft_solver_create", "deft_solver_destroy", "deft_solver_solve",
-    "deft_solver_last_kernel_ms",
+    "deft_solver_last_kernel_ms", "deft_solver_schedule",
     "deft_mem_alloc", "deft_mem_free", "deft_mem_open", "deft_mem_close",
     "deft_comm_flag_bytes", "deft_comm_create", "deft_comm_destroy",
     "deft_bucket_reduce_scatter", "deft_bucket_update", "deft_bucket_update_multi",
@@ -54,6 +54,9 @@ def _declare(lib):
         "deft_solver_solve": (c_i32, [c_vp, c_i32, P(c_i32), P(c_i64), P(c_i64),
                                       P(ctypes.c_uint8), P(c_i64)]),
         "deft_solver_last_kernel_ms": (c_f32, [c_vp]),
+        "deft_solver_schedule": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, P(c_i64), P(c_i64),
+                                         P(c_i64), P(c_i64), P(c_i32), c_i64, P(c_i64),
+                                         P(c_i32)]),
         "deft_mem_alloc": (c_i32, [c_sz, P(c_vp), P(ctypes.c_uint8)]),
         "deft_mem_free": (c_i32, [c_vp]),
         "deft_mem_open": (c_i32, [P(ctypes.c_uint8), P(c_vp)]),

@@ -513,3 +513,80 @@ extern "C" deft_status_t deft_bucket_update_multi(deft_comm* c, int32_t slot, in
   if (e != cudaSuccess) return cuda_fail(e, "update_allgather_multi_kernel");
   return DEFT_OK;
 }
+
+// ============================================================================
+// K5: persistent DeFT state machine (scheduler_kernel.cu)
+// ============================================================================
+extern "C" deft_status_t deft_solver_schedule(deft_solver* s, int32_t instances, int32_t n,
+                                              int32_t n_links, int32_t iterations,
+                                              const int64_t* comm, const int64_t* bwd,
+                                              const int64_t* fwd_caps,
+                                              const int64_t* bwd_caps, int32_t* out,
+                                              int64_t out_stride, int64_t* used,
+                                              int32_t* status) {
+  if (!s || instances <= 0 || n <= 0 || n_links <= 0 || iterations < 0)
+    return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_solver_schedule: bad arguments");
+  if (cudaSetDevice(s->device) != cudaSuccess) return fail(DEFT_ERR_CUDA, "cudaSetDevice");
+  int64_t words = 1;
+  for (int32_t i = 0; i < instances; ++i) {
+    int64_t dual = 0;
+    for (int32_t j = 0; j < n_links; ++j) dual += bwd_caps[(int64_t)i * n_links + j];
+    if (dual <= DEFT_MAX_EXACT_CAPACITY) words = std::max(words, (dual + 1 + 31) >> 5);
+  }
+  const size_t b_vec = align_up((size_t)(n + 1) * 8, 256);
+  const size_t b_caps = align_up((size_t)instances * n_links * 8, 256);
+  const size_t b_stat = align_up((size_t)instances * 4, 256);
+  const size_t b_used = align_up((size_t)instances * 8, 256);
+  const size_t b_out = align_up((size_t)instances * out_stride * 4, 256);
+  const size_t b_rows = align_up((size_t)instances * (n + 1) * words * 4, 256);
+  const size_t b_reach = align_up((size_t)instances * (n + 1) * 4, 256);
+  const size_t in_bytes = 2 * b_vec + 2 * b_caps + b_stat;
+  const size_t dev_bytes = in_bytes + b_used + b_out + b_rows + b_reach;
+  deft_status_t st = grow(s, in_bytes + b_used + b_out, dev_bytes);
+  if (st != DEFT_OK) return st;
+  char* h = s->pinned;
+  int64_t* hc = reinterpret_cast<int64_t*>(h);
+  int64_t* hb = reinterpret_cast<int64_t*>(h + b_vec);
+  hc[0] = hb[0] = 0;
+  memcpy(hc + 1, comm, (size_t)n * 8);
+  memcpy(hb + 1, bwd, (size_t)n * 8);
+  memcpy(h + 2 * b_vec, fwd_caps, (size_t)instances * n_links * 8);
+  memcpy(h + 2 * b_vec + b_caps, bwd_caps, (size_t)instances * n_links * 8);
+  memset(h + 2 * b_vec + 2 * b_caps, 0, (size_t)instances * 4);
+  char* d = s->dev;
+  DEFT_CUDA(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, s->stream));
+  SchedArgs A{};
+  A.n = n;
+  A.L = n_links;
+  A.T = iterations;
+  A.comm = reinterpret_cast<const int64_t*>(d);
+  A.bwd = reinterpret_cast<const int64_t*>(d + b_vec);
+  A.fcaps = reinterpret_cast<const int64_t*>(d + 2 * b_vec);
+  A.bcaps = reinterpret_cast<const int64_t*>(d + 2 * b_vec + b_caps);
+  A.status = reinterpret_cast<int32_t*>(d + 2 * b_vec + 2 * b_caps);
+  A.used = reinterpret_cast<int64_t*>(d + in_bytes);
+  A.out = reinterpret_cast<int32_t*>(d + in_bytes + b_used);
+  A.out_stride = out_stride;
+  A.rows = reinterpret_cast<uint32_t*>(d + in_bytes + b_used + b_out);
+  A.words = words;
+  A.reach = reinterpret_cast<int32_t*>(d + in_bytes + b_used + b_out + b_rows);
+  DEFT_CUDA(cudaEventRecord(s->ev0, s->stream));
+  cudaError_t e = launch_scheduler(A, instances, sched_smem_bytes(words), s->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "deft_scheduler_kernel");
+  DEFT_CUDA(cudaEventRecord(s->ev1, s->stream));
+  // status + used + records back in one copy (they are contiguous)
+  char* h_out = h + in_bytes;
+  DEFT_CUDA(cudaMemcpyAsync(h + 2 * b_vec + 2 * b_caps, A.status, (size_t)instances * 4,
+                            cudaMemcpyDeviceToHost, s->stream));
+  DEFT_CUDA(cudaMemcpyAsync(h_out, A.used, b_used + b_out, cudaMemcpyDeviceToHost, s->stream));
+  DEFT_CUDA(cudaStreamSynchronize(s->stream));
+  cudaEventElapsedTime(&s->last_ms, s->ev0, s->ev1);
+  memcpy(status, h + 2 * b_vec + 2 * b_caps, (size_t)instances * 4);
+  memcpy(used, h_out, (size_t)instances * 8);
+  for (int32_t i = 0; i < instances; ++i) {
+    const int64_t u = std::min<int64_t>(used[i], out_stride);
+    memcpy(out + (int64_t)i * out_stride, h_out + b_used + (size_t)i * out_stride * 4,
+           (size_t)u * 4);
+  }
+  return DEFT_OK;
+}

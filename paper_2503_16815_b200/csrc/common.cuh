@@ -89,6 +89,23 @@ cudaError_t launch_update_allgather_multi(const PeerPtrs& P, int rank, int world
                                           const int64_t* offsets, const int64_t* numels,
                                           float lr, float momentum, float grad_scale,
                                           float* mom, cudaStream_t stream);
+struct SchedArgs {
+  int32_t n, L, T;
+  const int64_t* comm;     // [n+1], by bucket id (index 0 unused)
+  const int64_t* bwd;      // [n+1] backward_us (only needed for the level caps)
+  const int64_t* fcaps;    // [instances][L] forward-stage link capacities
+  const int64_t* bcaps;    // [instances][L] backward-stage link capacities
+  uint32_t* rows;          // [instances][(n+1) * words]
+  int64_t words;           // row words for the largest dual capacity of the batch
+  int32_t* reach;          // [instances][n+1]
+  int32_t* out;            // [instances][out_stride] decision records
+  int64_t out_stride;
+  int32_t* status;         // [instances]
+  int64_t* used;           // [instances] ints written to `out`
+};
+int64_t sched_smem_bytes(int64_t words);
+cudaError_t launch_scheduler(const SchedArgs& a, int32_t instances, int64_t smem,
+                             cudaStream_t stream);
 cudaError_t launch_gather(char* dst, const void* const* srcs, const int64_t* dst_off,
                           const int64_t* lens, int32_t count, cudaStream_t stream);
 

@@ -1,0 +1,117 @@
+"""K5 front end: run whole DeFT schedules inside one persistent GPU kernel.
+
+``run_schedules`` takes a partitioned profile, a cluster and one capacity
+multiplier per instance, launches ``deft_scheduler_kernel`` once (one CTA per
+instance, csrc/scheduler_kernel.cu) and decodes its compact records into the
+same ``ScheduleDecision`` objects (``to_dict`` schema of scheduler.py:82-96 and
+the executor's ``exec`` notes) the host state machine produces.  Stage
+capacities are computed here with the reference's float expression and
+half-even ``round`` (scheduler.py:121-125), so the kernel is integer-only.
+Instances the kernel does not cover (scaled-mode capacities above 1e7 us)
+come back as None and are scheduled by the host state machine instead
+(which still solves every knapsack on the GPU).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from ._native import P, c_i32, c_i64
+from .errors import InternalInvariantError
+from .profiles import ClusterSpec, ModelProfile
+from .scheduler import (CapacityModel, Case, ExecNote, ScheduleDecision, Transfer,
+                        UpdateEvent)
+
+_HDR = 7
+_CASES = {1: Case.CASE1, 2: Case.CASE2, 3: Case.CASE3, 4: Case.CASE4}
+
+
+def _decode(rec: np.ndarray, n_used: int, names: list[str], all_ids: tuple[int, ...],
+            iterations: int) -> list[ScheduleDecision]:
+    out: list[ScheduleDecision] = []
+    r = rec[:n_used].tolist()
+    pos = 0
+    L = len(names)
+    for t in range(iterations):
+        for expect_stage in (0, 1):
+            stage, cas, n_tr, n_ev, merged, grad_uid, grad_merge = r[pos:pos + _HDR]
+            pos += _HDR
+            if stage != expect_stage:
+                raise InternalInvariantError("corrupt scheduler record stream")
+            trs = []
+            plans: list[list[int]] = [[] for _ in range(L)]
+            fresh = set()
+            for k in range(n_tr):
+                link, bid, grp, fr = r[pos + 4 * k:pos + 4 * k + 4]
+                trs.append(Transfer(link, bid, grp, bool(fr)))
+                plans[link].append(bid)
+                if fr:
+                    fresh.add(bid)
+            pos += 4 * n_tr
+            events, notes = [], []
+            for e in range(n_ev):
+                uid, first, k = r[pos + 3 * e:pos + 3 * e + 3]
+                origins = tuple(range(first, first + k))
+                events.append(UpdateEvent(origins, k))
+                notes.append((uid, k, origins))
+            pos += 3 * n_ev
+            plan = {nm: tuple(p) for nm, p in zip(names, plans)}
+            if stage == 0:
+                out.append(ScheduleDecision(
+                    iteration=t, stage="forward", forward_plan=plan, backward_plan={},
+                    fresh_ids=frozenset(), merged=(), update_events=(), case_taken=Case.CASE1,
+                    exec=ExecNote(transfers=tuple(trs))))
+            else:
+                out.append(ScheduleDecision(
+                    iteration=t, stage="backward", forward_plan={}, backward_plan=plan,
+                    fresh_ids=frozenset(fresh), merged=all_ids if merged else (),
+                    update_events=tuple(events), case_taken=_CASES[cas],
+                    exec=ExecNote(transfers=tuple(trs), grad_group=grad_uid,
+                                  grad_merge=bool(grad_merge), updates=tuple(notes))))
+    return out
+
+
+def run_schedules(profile: ModelProfile, cluster: ClusterSpec, multipliers: list[float],
+                  iterations: int) -> list[list[ScheduleDecision] | None]:
+    """One persistent launch for every multiplier; None for unsupported instances."""
+    solver = _native.subset_sum_solver()
+    n = profile.n_buckets
+    L = len(cluster.links)
+    inst = len(multipliers)
+    comm = np.array([b.comm_fast_us for b in profile.buckets], dtype=np.int64)
+    bwd = np.array([b.backward_us for b in profile.buckets], dtype=np.int64)
+    fc, bc = [], []
+    for m in multipliers:
+        cm = CapacityModel.from_profile(profile, cluster, m)
+        fc.extend(cm.stage_capacities("forward"))
+        bc.extend(cm.stage_capacities("backward"))
+    fcaps = np.array(fc, dtype=np.int64)
+    bcaps = np.array(bc, dtype=np.int64)
+    stride = iterations * 2 * (_HDR + 8 * n + 12) + 16
+    out = np.zeros(inst * stride, dtype=np.int32)
+    used = np.zeros(inst, dtype=np.int64)
+    status = np.zeros(inst, dtype=np.int32)
+    st = _native.lib().deft_solver_schedule(
+        solver._h, inst, n, L, iterations, comm.ctypes.data_as(P(c_i64)),
+        bwd.ctypes.data_as(P(c_i64)), fcaps.ctypes.data_as(P(c_i64)),
+        bcaps.ctypes.data_as(P(c_i64)), out.ctypes.data_as(P(c_i32)), stride,
+        used.ctypes.data_as(P(c_i64)), status.ctypes.data_as(P(c_i32)))
+    _native.check(st, "deft_solver_schedule")
+    solver.kernel_ms += float(_native.lib().deft_solver_last_kernel_ms(solver._h))
+    names = [l.name for l in cluster.links]
+    all_ids = tuple(b.id for b in profile.buckets)
+    res: list[list[ScheduleDecision] | None] = []
+    for i in range(inst):
+        if status[i] == -4:
+            res.append(None)
+            continue
+        if status[i] == -6:
+            raise InternalInvariantError("insufficient capacity yet queue drained")
+        if status[i] != 0:
+            raise InternalInvariantError(f"scheduler kernel status {status[i]}")
+        res.append(_decode(out[i * stride:(i + 1) * stride], int(used[i]), names, all_ids,
+                           iterations))
+    return res
+
+
+__all__ = ["run_schedules"]
