@@ -527,11 +527,14 @@ extern "C" deft_status_t deft_solver_schedule(deft_solver* s, int32_t instances,
   if (!s || instances <= 0 || n <= 0 || n_links <= 0 || iterations < 0)
     return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_solver_schedule: bad arguments");
   if (cudaSetDevice(s->device) != cudaSuccess) return fail(DEFT_ERR_CUDA, "cudaSetDevice");
-  int64_t words = 1;
+  int64_t words = 1, smem_words = 0;
   for (int32_t i = 0; i < instances; ++i) {
     int64_t dual = 0;
     for (int32_t j = 0; j < n_links; ++j) dual += bwd_caps[(int64_t)i * n_links + j];
-    if (dual <= DEFT_MAX_EXACT_CAPACITY) words = std::max(words, (dual + 1 + 31) >> 5);
+    if (dual > DEFT_MAX_EXACT_CAPACITY) continue;
+    const int64_t w = (dual + 1 + 31) >> 5;
+    words = std::max(words, w);
+    if (w <= smem_words_limit()) smem_words = std::max(smem_words, w);
   }
   const size_t b_vec = align_up((size_t)(n + 1) * 8, 256);
   const size_t b_caps = align_up((size_t)instances * n_links * 8, 256);
@@ -570,8 +573,9 @@ extern "C" deft_status_t deft_solver_schedule(deft_solver* s, int32_t instances,
   A.rows = reinterpret_cast<uint32_t*>(d + in_bytes + b_used + b_out);
   A.words = words;
   A.reach = reinterpret_cast<int32_t*>(d + in_bytes + b_used + b_out + b_rows);
+  A.smem_row_words = smem_words;
   DEFT_CUDA(cudaEventRecord(s->ev0, s->stream));
-  cudaError_t e = launch_scheduler(A, instances, sched_smem_bytes(words), s->stream);
+  cudaError_t e = launch_scheduler(A, instances, sched_smem_bytes(smem_words), s->stream);
   if (e != cudaSuccess) return cuda_fail(e, "deft_scheduler_kernel");
   DEFT_CUDA(cudaEventRecord(s->ev1, s->stream));
   // status + used + records back in one copy (they are contiguous)

@@ -102,6 +102,7 @@ struct SchedArgs {
   int64_t out_stride;
   int32_t* status;         // [instances]
   int64_t* used;           // [instances] ints written to `out`
+  int64_t smem_row_words;  // row words the launch's dynamic shared memory can hold
 };
 int64_t sched_smem_bytes(int64_t words);
 cudaError_t launch_scheduler(const SchedArgs& a, int32_t instances, int64_t smem,

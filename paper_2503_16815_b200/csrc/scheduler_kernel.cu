@@ -27,8 +27,6 @@
 
 namespace deft {
 
-__device__ __forceinline__ int64_t smem_words_limit_dev() { return 56 * 1024; }
-
 constexpr int kSchedThreads = 1024;
 constexpr int kSchedMaxN = 1024;
 constexpr int kSchedMaxLinks = 4;
@@ -90,7 +88,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) deft_scheduler_kernel(SchedA
   // ---- phase 1: suffix rows over ascending ids 1..n for capacity C -------------
   // (the in-place top-down chunked update of subset_sum_kernel while the row
   // fits in shared memory; above that, row i is built from the stored row i+1)
-  const bool in_smem = words <= smem_words_limit_dev();
+  const bool in_smem = words <= a.smem_row_words;
   if (C > 0) {
     if (tid == 0) {
       if (in_smem) smem_row[0] = 1u;
@@ -417,8 +415,10 @@ __global__ void __launch_bounds__(kSchedThreads, 1) deft_scheduler_kernel(SchedA
   }
 }
 
+// dynamic shared memory of a launch: the largest row that fits (instances with
+// longer rows use the global-row path) or the bookkeeping state, whichever is larger
 int64_t sched_smem_bytes(int64_t words) {
-  const int64_t row = words <= smem_words_limit() ? words * 4 : 0;
+  const int64_t row = (words < smem_words_limit() ? words : smem_words_limit()) * 4;
   const int64_t state = (int64_t)sizeof(SchedState);
   return row > state ? row : state;
 }

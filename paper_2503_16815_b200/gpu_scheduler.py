@@ -71,8 +71,44 @@ def _decode(rec: np.ndarray, n_used: int, names: list[str], all_ids: tuple[int, 
     return out
 
 
+class KernelSchedule:
+    """The records of one scheduler instance; decoded on demand (the feedback loop
+    only needs the merge counts of most attempts)."""
+
+    def __init__(self, rec: np.ndarray, used: int, names, all_ids, iterations: int):
+        self._rec = rec[:used].copy()
+        self._names, self._all_ids, self._iterations = names, all_ids, iterations
+        self._decoded: list[ScheduleDecision] | None = None
+
+    def merge_counts(self) -> list[int]:
+        """merge_count of every update event, in stream order (preserver.py:129-134)."""
+        r = self._rec
+        ks, pos = [], 0
+        for _ in range(2 * self._iterations):
+            n_tr, n_ev = int(r[pos + 2]), int(r[pos + 3])
+            pos += _HDR + 4 * n_tr
+            for e in range(n_ev):
+                ks.append(int(r[pos + 3 * e + 2]))
+            pos += 3 * n_ev
+        return ks
+
+    def decisions(self) -> list[ScheduleDecision]:
+        if self._decoded is None:
+            self._decoded = _decode(self._rec, len(self._rec), self._names, self._all_ids,
+                                    self._iterations)
+        return self._decoded
+
+
 def run_schedules(profile: ModelProfile, cluster: ClusterSpec, multipliers: list[float],
                   iterations: int) -> list[list[ScheduleDecision] | None]:
+    """One persistent launch for every multiplier; decoded decision lists, None for
+    unsupported instances."""
+    return [None if k is None else k.decisions()
+            for k in run_schedules_lazy(profile, cluster, multipliers, iterations)]
+
+
+def run_schedules_lazy(profile: ModelProfile, cluster: ClusterSpec, multipliers: list[float],
+                       iterations: int) -> list[KernelSchedule | None]:
     """One persistent launch for every multiplier; None for unsupported instances."""
     solver = _native.subset_sum_solver()
     n = profile.n_buckets
@@ -100,7 +136,7 @@ def run_schedules(profile: ModelProfile, cluster: ClusterSpec, multipliers: list
     solver.kernel_ms += float(_native.lib().deft_solver_last_kernel_ms(solver._h))
     names = [l.name for l in cluster.links]
     all_ids = tuple(b.id for b in profile.buckets)
-    res: list[list[ScheduleDecision] | None] = []
+    res: list[KernelSchedule | None] = []
     for i in range(inst):
         if status[i] == -4:
             res.append(None)
@@ -109,9 +145,9 @@ def run_schedules(profile: ModelProfile, cluster: ClusterSpec, multipliers: list
             raise InternalInvariantError("insufficient capacity yet queue drained")
         if status[i] != 0:
             raise InternalInvariantError(f"scheduler kernel status {status[i]}")
-        res.append(_decode(out[i * stride:(i + 1) * stride], int(used[i]), names, all_ids,
-                           iterations))
+        res.append(KernelSchedule(out[i * stride:(i + 1) * stride], int(used[i]), names,
+                                  all_ids, iterations))
     return res
 
 
-__all__ = ["run_schedules"]
+__all__ = ["run_schedules", "run_schedules_lazy", "KernelSchedule"]
