@@ -71,7 +71,8 @@ def main():
             prof = prof.scaled_comm(1.0 / bw)
         cfg = D.PartitionConfig(6_500_000, mu=1.65)
         # K5: every attempt in one persistent scheduler kernel
-        D.feedback_loop(prof, cluster, cfg, walk, iterations=20, engine="kernel")  # warm
+        from paper_2503_16815_b200 import gpu_scheduler
+        gpu_scheduler.run_schedules_lazy(D.partition_buckets(prof, cfg), cluster, [1.0], 4)
         k0 = solver.kernel_ms
         t0 = time.perf_counter()
         sched_k, verdict_k = D.feedback_loop(prof, cluster, cfg, walk, iterations=200,
