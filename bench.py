@@ -216,6 +216,40 @@ def cpu_reference_run(model_name, steps, warmup, batch):
 
 # ----------------------------------------------------------------- GPU path
 
+def solver_measurement():
+    """The scheduling side of the path: DeFT's feedback loop (200 iterations, up to
+    10 capacity retries) on the reference's ResNet-101 fixture at quarter bandwidth
+    -- the persistent GPU state machine (K5) vs the CPU oracle port (1 core)."""
+    import paper_2503_16815_b200 as D
+    from paper_2503_16815_b200 import gpu_scheduler
+    from oracle import deft_oracle as O
+    inputs = json.loads((ROOT / "tests" / "golden" / "inputs.json").read_text())
+    walk = D.WalkParams.from_dict(inputs["walk"])
+    cl = inputs["clusters"]["dual"]
+    prof = D.profile_from_dict(inputs["profiles"]["resnet101"]).scaled_comm(4.0)
+    cfg = D.PartitionConfig(6_500_000, mu=1.65)
+    gpu_scheduler.run_schedules_lazy(D.partition_buckets(prof, cfg),
+                                     D.cluster_from_dict(cl), [1.0], 4)   # warm
+    t0 = time.perf_counter()
+    sched, verdict = D.feedback_loop(prof, D.cluster_from_dict(cl), cfg, walk, iterations=200)
+    t_gpu = time.perf_counter() - t0
+    b = O.scaled_comm(inputs["profiles"]["resnet101"]["buckets"], 4.0)
+    part = O.partition(b, sum(x["forward_us"] for x in b), 6_500_000, 1.65)
+    t0 = time.perf_counter()
+    m = 1.0
+    for _ in range(verdict.retries + 1):
+        dec = O.schedule(part, [l["speed_ratio_to_fast"] for l in cl["links"]],
+                         [l["name"] for l in cl["links"]], 200, m)
+        m *= 1.1
+    t_cpu = time.perf_counter() - t0
+    same = O.jsonl(dec) == "".join(l + "\n" for l in sched.jsonl_lines())
+    return {"workload": "feedback_loop, ResNet-101 fixture, dual link, bw x0.25, 200 iterations",
+            "retries": verdict.retries, "gpu_s": round(t_gpu, 4),
+            "oracle_cpu_s_1core": round(t_cpu, 3),
+            "reference_python_s": 8.4, "reference_src": "BASELINE.md (build container)",
+            "streams_identical": same}
+
+
 def compute_only_step_ms(model, batch, loss_fn, steps, warmup, world, dist, device):
     """The compute roofline of SURVEY 8d: one GPU's fwd + bwd + fused SGD/momentum
     step with NO communication, CUDA-graphed like the DeFT step."""
@@ -551,6 +585,12 @@ def main():
             else "B200_PROFILING.md measured peer copy 770 GB/s",
             "isolated": iso, "in_step": ks}
 
+    solver = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            solver = solver_measurement()
+        except Exception as e:  # reported, never fatal
+            solver = {"error": repr(e)}
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -589,6 +629,7 @@ def main():
             "frac_of_compute_roofline": round(ms_compute / ms_step, 4),
             "roofline": roof,
             "cpu_baseline": cpu_base,
+            "solver": solver,
             "clocks": clk.summary(),
         }
         print(json.dumps(line))
