@@ -363,6 +363,22 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
     return out
 
 
+def init_quiet(dist, device):
+    """NCCL prints its version banner on fd 1 when the communicator comes up;
+    rank 0's stdout must carry exactly one JSON line, so point fd 1 at stderr
+    while the process group (eagerly, device_id given) initialises."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        dist.init_process_group("nccl", device_id=device)
+        dist.barrier()
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
+
+
 def ddp_baseline(args, world, rank, device, dist):
     """NCCL WFBP baseline: torch DistributedDataParallel (bucketed all-reduce
     overlapped with backward, every iteration) + fused SGD/momentum, eager."""
@@ -445,7 +461,7 @@ def main():
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        init_quiet(dist, device)
     torch.backends.cudnn.benchmark = True
     if args.impl == "ddp":
         return ddp_baseline(args, world, rank, device, dist)
