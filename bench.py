@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs")
     ap.add_argument("--bucket-mb", type=float, default=None,
                     help="partition size in MB of fp32 (default: the reference's 6.5M params)")
+    ap.add_argument("--links", default="both", choices=["both", "sm", "ce"],
+                    help="NVLink channels the schedule may use (both = measured SM + CE)")
     ap.add_argument("--dump-profile", default=None,
                     help="write the B200-measured ModelProfile + ClusterSpec JSON here")
     ap.add_argument("--comm-scale", type=float, default=1.0,
@@ -252,7 +254,8 @@ def solver_measurement():
 
 def compute_only_step_ms(model, batch, loss_fn, steps, warmup, world, dist, device):
     """The compute roofline of SURVEY 8d: one GPU's fwd + bwd + fused SGD/momentum
-    step with NO communication, CUDA-graphed like the DeFT step."""
+    step with NO communication -- the faster of eager and CUDA-graphed execution
+    (models differ: ResNet-101 gains from graphs, GPT-2 loses)."""
     import torch
     params = [p for p in model.parameters() if p.requires_grad]
     opt = torch.optim.SGD(params, lr=0.1, momentum=0.9, fused=True)
@@ -267,36 +270,42 @@ def compute_only_step_ms(model, batch, loss_fn, steps, warmup, world, dist, devi
         opt.step()
         return loss.detach()
 
+    def timed(fn):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
         for _ in range(3):
             step()
     s.synchronize()
+    ms_eager = timed(step)
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         step()
-    for _ in range(warmup):
-        g.replay()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(steps):
-        g.replay()
-    b.record()
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / steps
-    if world > 1:
-        t = torch.tensor([ms], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms_graph = timed(g.replay)
     del g, opt
     for p in params:
         p.grad = None
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
-    return ms
+    return min(ms_eager, ms_graph), {"eager_ms": round(ms_eager, 3),
+                                     "graph_ms": round(ms_graph, 3)}
 
 
 def isolated_kernels(ddp, world, dist, device, reps=10):
@@ -361,6 +370,11 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
     ddp.mom.copy_(saved_m)
     torch.cuda.synchronize()
     return out
+
+
+def _native_channel(name):
+    from paper_2503_16815_b200 import _native
+    return _native.CHANNEL_SM if name == "sm" else _native.CHANNEL_CE
 
 
 def init_quiet(dist, device):
@@ -472,14 +486,15 @@ def main():
     batch = make_batch(args.model, args.batch, device, seed=1234 + rank)
 
     # 1) compute roofline: no communication at all
-    ms_compute = compute_only_step_ms(model, batch, loss_fn, args.steps, args.warmup, world,
-                                      dist, device)
+    ms_compute, compute_modes = compute_only_step_ms(model, batch, loss_fn, args.steps,
+                                                     args.warmup, world, dist, device)
 
     # 2) DeFT: profile on this GPU, plan (partition + feedback loop), run
     walk = D.WalkParams.from_dict(
         json.loads((ROOT / "tests" / "golden" / "inputs.json").read_text())["walk"])
     psize = 6_500_000 if args.bucket_mb is None else int(args.bucket_mb * 2**20 / 4)
-    cfg = D.DeftConfig(lr=0.1, momentum=0.9, walk=walk, cuda_graphs=not args.eager,
+    cfg = D.DeftConfig(lr=0.1, momentum=0.9, walk=walk,
+                       cuda_graphs=False if args.eager else "auto",
                        update_placement=args.update_placement,
                        autocast_dtype=None if args.model == "gpt2" else torch.bfloat16,
                        partition=D.PartitionConfig(partition_size=psize, mu=1.0))
@@ -492,7 +507,12 @@ def main():
             indent=1, sort_keys=True))
     if args.comm_scale != 1.0:
         prof = prof.scaled_comm(args.comm_scale)
-    part = ddp.plan(prof, ddp.cluster)
+    cluster = ddp.cluster
+    if args.links != "both" and world > 1:
+        cluster = D.ClusterSpec(links=(D.LinkSpec(f"nvlink_{args.links}", 1.0),))
+        ddp.channel_of_link = [_native_channel(args.links)]
+        ddp.cluster = cluster
+    part = ddp.plan(prof, cluster)
     t_setup = time.perf_counter() - t_setup
 
     def timed(step_fn, k):
@@ -633,7 +653,8 @@ def main():
                        "partition_size": psize, "comm_scale": args.comm_scale,
                        "merge_counts": sorted({u.merge_count for pair in ddp.decision_log
                                                for d in pair for u in d.update_events}),
-                       "cuda_graphs": ddp.cfg.cuda_graphs, "graphs_captured": len(ddp._graphs),
+                       "cuda_graphs": ddp.cfg.cuda_graphs, "graph_choice": ddp.graph_choice,
+                       "graphs_captured": len(ddp._graphs),
                        "warmup_steps_run": warm, "setup_s": round(t_setup, 2)},
             "e2e": {"value": round(e2e_value, 2), "unit": "samples/s",
                     "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": 4,
@@ -641,6 +662,7 @@ def main():
                             "overlaps step t); loss D2H every step"},
             "gpu_launches": int(launches),
             "compute_only_ms_per_step": round(ms_compute, 3),
+            "compute_only_modes": compute_modes,
             "exposed_comm_ms": round(ms_step - ms_compute, 3),
             "frac_of_compute_roofline": round(ms_compute / ms_step, 4),
             "roofline": roof,

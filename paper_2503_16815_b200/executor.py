@@ -61,7 +61,9 @@ class DeftConfig:
     lookahead: int = 32                     # decisions generated ahead of execution
     use_ce_channel: bool = True             # second link = copy engines
     instrument: bool = False                # CUDA events around every native launch
-    cuda_graphs: bool = True                # capture + replay each distinct iteration shape
+    # capture + replay each distinct iteration shape; "auto" = keep graphs only if
+    # warm_up() measures them faster than eager execution
+    cuda_graphs: bool | str = "auto"
     # where the delayed update of bucket b runs inside its no-read window:
     # "bucket" = right after b's backward (overlaps the rest of the backward),
     # "end" = after the whole backward (one launch per event at W == 1),
@@ -339,11 +341,13 @@ class DeftDataParallel:
         self._in_step = False
         # CUDA graphs: iterations run strictly one after another (side streams
         # join the compute stream at the end of each iteration)
-        self._sequential = self.cfg.cuda_graphs
+        self._sequential = bool(self.cfg.cuda_graphs)
+        self._use_graphs = bool(self.cfg.cuda_graphs)
+        self.graph_choice = None
         self._graphs: dict = {}
         self._seen: dict = {}
         self._static = None
-        self._pool = torch.cuda.graph_pool_handle() if self.cfg.cuda_graphs else None
+        self._pool = torch.cuda.graph_pool_handle() if self._use_graphs else None
         self._captured_native = 0
         self._replayed_native = 0
         self.last_step_kind = None
@@ -368,7 +372,7 @@ class DeftDataParallel:
             return torch.autocast("cuda", enabled=False)
         # the weight-cast cache must not outlive a CUDA-graph capture
         return torch.autocast("cuda", dtype=self.cfg.autocast_dtype,
-                              cache_enabled=not self.cfg.cuda_graphs)
+                              cache_enabled=not getattr(self, "_sequential", False))
 
     def _bind_grads(self, slot: int):
         if self._bound_slot == slot:
@@ -623,21 +627,52 @@ class DeftDataParallel:
         return loss
 
     def warm_up(self, batch, loss_fn: Callable, min_steps: int = 3, max_steps: int = 64,
-                steady: int = 6) -> int:
+                steady: int = 6, compare: int = 4) -> int:
         """Run steps until the last `steady` were all graph replays (every
-        steady-state iteration shape captured); returns the number of steps run."""
+        steady-state iteration shape captured).  Then, with ``cuda_graphs="auto"``,
+        time `compare` replayed steps against `compare` eager ones and keep the
+        faster mode (some models' captured kernels are slower than their eager
+        ones).  Returns the number of steps run."""
         streak, n = 0, 0
         while n < max_steps and (n < min_steps or streak < steady):
             self.train_step(batch, loss_fn)
             n += 1
             streak = streak + 1 if self.last_step_kind == "replay" else 0
-            if not self._sequential:
+            if not self._use_graphs:
                 streak = steady
+        if self.cfg.cuda_graphs == "auto" and self._use_graphs and compare > 0:
+            t_graph = self._time_steps(batch, loss_fn, compare)
+            self._use_graphs = False
+            t_eager = self._time_steps(batch, loss_fn, compare)
+            self._use_graphs = t_graph <= t_eager
+            self.graph_choice = {"graph_ms": t_graph / compare, "eager_ms": t_eager / compare,
+                                 "use_graphs": self._use_graphs}
+            n += 2 * compare
         return n
 
+    def _time_steps(self, batch, loss_fn, k) -> float:
+        ms = 0.0
+        if self.world > 1:
+            torch.distributed.barrier(group=self.group)
+        torch.cuda.synchronize(self.device)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(k):
+            self.train_step(batch, loss_fn)
+        b.record()
+        torch.cuda.synchronize(self.device)
+        ms = a.elapsed_time(b)
+        if self.world > 1:   # every rank must take the same decision
+            t = torch.tensor([ms], device=self.device)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX, group=self.group)
+            ms = float(t.item())
+        return ms
+
     def _dispatch(self, it: IterPlan, batch, loss_fn: Callable) -> torch.Tensor:
-        if not self._sequential or self.cfg.instrument:
+        if not self._sequential or self.cfg.instrument or not self._use_graphs:
             self.last_step_kind = "eager"
+            if self._sequential and self._static is not None:
+                batch = self._static_inputs(batch)
             return self._run_iteration(it, batch, loss_fn)
         static = self._static_inputs(batch)
         hit = self._graphs.get(it.key)
