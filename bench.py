@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=None,
                     help="per-GPU batch (default 64; GPT-2: 16 sequences of 1024)")
     ap.add_argument("--update-placement", default="end", choices=["bucket", "end", "start"])
+    ap.add_argument("--update-blocks", type=int, default=0,
+                    help="CTA budget of the update kernels (0 = default)")
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs")
     ap.add_argument("--bucket-mb", type=float, default=None,
                     help="partition size in MB of fp32 (default: the reference's 6.5M params)")
@@ -496,6 +498,7 @@ def main():
     cfg = D.DeftConfig(lr=0.1, momentum=0.9, walk=walk,
                        cuda_graphs=False if args.eager else "auto",
                        update_placement=args.update_placement,
+                       update_blocks=args.update_blocks,
                        autocast_dtype=None if args.model == "gpt2" else torch.bfloat16,
                        partition=D.PartitionConfig(partition_size=psize, mu=1.0))
     ddp = D.DeftDataParallel(model, cfg)

@@ -126,6 +126,8 @@ deft_status_t deft_comm_create(int32_t rank, int32_t world, void* const* grads,
                                int64_t slot_elems, int32_t n_slots, int32_t grad_dtype,
                                deft_comm** out);
 deft_status_t deft_comm_destroy(deft_comm* c);
+/* CTA budget of the update kernels (0 = default); must be equal on every rank. */
+deft_status_t deft_comm_set_update_blocks(deft_comm* c, int32_t blocks);
 
 /* grad_dtype codes */
 #define DEFT_DTYPE_F32 0

@@ -118,6 +118,11 @@ class BucketComm:
                                                        c_vp(stream.cuda_stream)),
               "deft_bucket_reduce_scatter")
 
+    def set_update_blocks(self, blocks: int) -> None:
+        """CTA budget of the update kernels (0 = default); identical on every rank."""
+        check(_native.lib().deft_comm_set_update_blocks(self._h, int(blocks)),
+              "deft_comm_set_update_blocks")
+
     def update(self, slot: int, offset: int, numel: int, lr: float, momentum: float,
                grad_scale: float, mom: torch.Tensor, stream) -> None:
         check(_native.lib().deft_bucket_update(self._h, slot, offset, numel, lr, momentum,

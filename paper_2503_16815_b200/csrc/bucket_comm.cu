@@ -427,9 +427,10 @@ static void upd_dispatch(int world, int grid, cudaStream_t stream, const PeerPtr
 cudaError_t launch_update_allgather(const PeerPtrs& P, int rank, int world, int dtype,
                                     int64_t slot_base, int64_t offset, int64_t numel, float lr,
                                     float momentum, float grad_scale, float* mom,
-                                    cudaStream_t stream) {
+                                    int max_blocks, cudaStream_t stream) {
   const ShardRange sh = shard_of(offset, numel, rank, world, dtype == 0 ? 4 : 8);
-  const int grid = comm_grid_for((numel + world - 1) / world);
+  int grid = comm_grid_for((numel + world - 1) / world);
+  if (max_blocks > 0 && grid > max_blocks) grid = max_blocks;
   if (dtype == 0)
     upd_dispatch<float>(world, grid, stream, P, rank, slot_base, sh.lo, sh.hi, lr, momentum,
                         grad_scale, mom);
@@ -676,7 +677,7 @@ cudaError_t launch_update_allgather_multi(const PeerPtrs& P, int rank, int world
                                           int64_t slot_base, int32_t count,
                                           const int64_t* offsets, const int64_t* numels,
                                           float lr, float momentum, float grad_scale,
-                                          float* mom, cudaStream_t stream) {
+                                          float* mom, int max_blocks, cudaStream_t stream) {
   const int align = dtype == 0 ? 4 : 8;
   for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
     SegTable t{};
@@ -696,6 +697,7 @@ cudaError_t launch_update_allgather_multi(const PeerPtrs& P, int rank, int world
     }
     // identical on every rank: depends on the bucket sizes, not on this rank's shards
     int grid = comm_grid_for((total_elems + world - 1) / world);
+    if (max_blocks > 0 && grid > max_blocks) grid = max_blocks;
 #define DEFT_UPM_CASE(WW)                                                                   \
   case WW:                                                                                  \
     if (dtype == 0)                                                                         \

@@ -319,6 +319,7 @@ struct deft_comm {
   PeerPtrs P{};
   char* staging = nullptr;  // CE channel: (W-1) peer shards
   size_t staging_bytes = 0;
+  int update_blocks = 0;    // CTA budget of the update kernels (0 = comm default)
 };
 
 extern "C" size_t deft_comm_flag_bytes(int32_t world) {
@@ -353,6 +354,13 @@ extern "C" deft_status_t deft_comm_create(int32_t rank, int32_t world, void* con
     }
   }
   *out = c;
+  return DEFT_OK;
+}
+
+extern "C" deft_status_t deft_comm_set_update_blocks(deft_comm* c, int32_t blocks) {
+  if (!c || blocks < 0 || blocks > kMaxCommBlocks)
+    return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_comm_set_update_blocks");
+  c->update_blocks = blocks;
   return DEFT_OK;
 }
 
@@ -438,7 +446,8 @@ extern "C" deft_status_t deft_bucket_update(deft_comm* c, int32_t slot, int64_t 
     return DEFT_OK;
   }
   cudaError_t e = launch_update_allgather(c->P, c->rank, c->world, c->dtype, slot_base, offset,
-                                          numel, lr, momentum, grad_scale, d_mom, s);
+                                          numel, lr, momentum, grad_scale, d_mom,
+                                          c->update_blocks, s);
   if (e != cudaSuccess) return cuda_fail(e, "update_allgather_kernel");
   return DEFT_OK;
 }
@@ -509,7 +518,7 @@ extern "C" deft_status_t deft_bucket_update_multi(deft_comm* c, int32_t slot, in
   }
   cudaError_t e = launch_update_allgather_multi(c->P, c->rank, c->world, c->dtype, slot_base,
                                                 count, offsets, numels, lr, momentum, grad_scale,
-                                                d_mom, s);
+                                                d_mom, c->update_blocks, s);
   if (e != cudaSuccess) return cuda_fail(e, "update_allgather_multi_kernel");
   return DEFT_OK;
 }

@@ -78,7 +78,7 @@ cudaError_t launch_ce_reduce(char* own_grad_slot, const char* staging, int dtype
 cudaError_t launch_update_allgather(const PeerPtrs& P, int rank, int world, int dtype,
                                     int64_t slot_base, int64_t offset, int64_t numel, float lr,
                                     float momentum, float grad_scale, float* mom,
-                                    cudaStream_t stream);
+                                    int max_blocks, cudaStream_t stream);
 cudaError_t launch_sgd_local(const void* grad, int dtype, void* param, float* master,
                              float* mom, int32_t count, const int64_t* offsets, const int64_t* numels,
                              const float* scales, float lr, float momentum,
@@ -88,7 +88,7 @@ cudaError_t launch_update_allgather_multi(const PeerPtrs& P, int rank, int world
                                           int64_t slot_base, int32_t count,
                                           const int64_t* offsets, const int64_t* numels,
                                           float lr, float momentum, float grad_scale,
-                                          float* mom, cudaStream_t stream);
+                                          float* mom, int max_blocks, cudaStream_t stream);
 struct SchedArgs {
   int32_t n, L, T;
   const int64_t* comm;     // [n+1], by bucket id (index 0 unused)

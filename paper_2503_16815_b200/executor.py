@@ -70,6 +70,9 @@ class DeftConfig:
     # "start" = at the start of the iteration it becomes visible in, input-side
     #           bucket first, each bucket's forward waiting only for its own update
     update_placement: str = "end"
+    # CTAs of every update kernel (0 = the comm default).  With "start" placement a
+    # small budget lets the update overlap the forward instead of displacing it.
+    update_blocks: int = 0
     graph_warmup: int = 1                   # eager runs of a shape before it is captured
 
 
@@ -331,6 +334,8 @@ class DeftDataParallel:
         self._gather_slot = None
         self.scheduler = DeftScheduler(part, cluster, mult)
         self.capacity_multiplier = mult
+        blocks = self.cfg.update_blocks or (24 if self.cfg.update_placement == "start" else 0)
+        self.comm.set_update_blocks(blocks)
         self.planner = ExecutionPlanner(self.scheduler, self.cfg.n_slots, self.cfg.lookahead,
                                         lag=2 if self.cfg.update_placement == "start" else 1)
         self.link_streams = [torch.cuda.Stream(self.device) for _ in cluster.links]
@@ -643,11 +648,13 @@ class DeftDataParallel:
         if self.cfg.cuda_graphs == "auto" and self._use_graphs and compare > 0:
             t_graph = self._time_steps(batch, loss_fn, compare)
             self._use_graphs = False
+            for _ in range(2):                    # eager warm-up: allocator, autotuning
+                self.train_step(batch, loss_fn)
             t_eager = self._time_steps(batch, loss_fn, compare)
             self._use_graphs = t_graph <= t_eager
             self.graph_choice = {"graph_ms": t_graph / compare, "eager_ms": t_eager / compare,
                                  "use_graphs": self._use_graphs}
-            n += 2 * compare
+            n += 2 * compare + 2
         return n
 
     def _time_steps(self, batch, loss_fn, k) -> float:
