@@ -44,7 +44,8 @@ def parse():
                          "NCCL WFBP baseline)")
     ap.add_argument("--batch", type=int, default=None,
                     help="per-GPU batch (default 64; GPT-2: 16 sequences of 1024)")
-    ap.add_argument("--update-placement", default="end", choices=["bucket", "end", "start"])
+    ap.add_argument("--update-placement", default="auto",
+                    choices=["auto", "bucket", "end", "start"])
     ap.add_argument("--update-blocks", type=int, default=0,
                     help="CTA budget of the update kernels (0 = default)")
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs")
@@ -337,7 +338,7 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
             t = torch.tensor([ms], device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        n = 1 if (kind == "update" and ddp.cfg.update_placement == "end") else len(ddp.buckets)
+        n = 1 if (kind == "update" and ddp.placement == "end") else len(ddp.buckets)
         out[kind] = {"launches": n, "ms_per_pass": round(ms, 4),
                      "avg_launch_us": round(ms / n * 1e3, 2), "bytes_per_pass": nbytes,
                      "achieved_gbs": round(nbytes / (ms / 1e3) / 1e9, 1)}
@@ -352,7 +353,7 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
         upd_bytes = sum((b.hi - b.lo) * esz * (world - 1) // world for b in ddp.buckets)
 
     def updates():
-        if ddp.cfg.update_placement == "end":   # the step's own launch shape
+        if ddp.placement == "end":   # the step's own launch shape
             ddp.comm.update_multi(slot, [(b.lo, b.hi) for b in ddp.buckets], 1.0, 0.0, 0.9,
                                   ddp.mom, s)
             return
@@ -605,7 +606,7 @@ def main():
         in_step = (r["bytes"] / r["launches"]) / (avg_ms / 1e3) / 1e9
     achieved = iso[kind]["achieved_gbs"]
     upd_name = "sgd_local_kernel" if world == 1 else (
-        "update_allgather_multi_kernel" if ddp.cfg.update_placement == "end"
+        "update_allgather_multi_kernel" if ddp.placement == "end"
         else "update_allgather_kernel")
     roof = {"kernel": {"update": upd_name,
                        "reduce_scatter": "reduce_scatter_kernel"}[kind],
@@ -650,7 +651,7 @@ def main():
                        "parallelism": f"dp{world}", "l2": "working set (activations) >> L2 126 MB",
                        "grad_dtype": str(ddp.cfg.grad_dtype).replace("torch.", ""),
                        "compute": "bf16 autocast" if args.model != "gpt2" else "bf16 weights",
-                       "update_placement": ddp.cfg.update_placement,
+                       "update_placement": ddp.placement,
                        "buckets": part.n_buckets, "links": [l.name for l in ddp.cluster.links],
                        "capacity_multiplier": ddp.capacity_multiplier,
                        "partition_size": psize, "comm_scale": args.comm_scale,

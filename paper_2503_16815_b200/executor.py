@@ -64,14 +64,16 @@ class DeftConfig:
     # capture + replay each distinct iteration shape; "auto" = keep graphs only if
     # warm_up() measures them faster than eager execution
     cuda_graphs: bool | str = "auto"
-    # where the delayed update of bucket b runs inside its no-read window:
+    # where the delayed update of bucket b runs inside its no-read window
+    # ("auto": "end" on one GPU, "start" on several -- measured best):
     # "bucket" = right after b's backward (overlaps the rest of the backward),
     # "end" = after the whole backward (one launch per event at W == 1),
     # "start" = at the start of the iteration it becomes visible in, input-side
     #           bucket first, each bucket's forward waiting only for its own update
-    update_placement: str = "end"
-    # CTAs of every update kernel (0 = the comm default).  With "start" placement a
-    # small budget lets the update overlap the forward instead of displacing it.
+    update_placement: str = "auto"
+    # CTAs of every update kernel (0 = the comm default; 16 with "start").  With
+    # "start" placement a small budget lets the update overlap the forward instead
+    # of displacing it.
     update_blocks: int = 0
     graph_warmup: int = 1                   # eager runs of a shape before it is captured
 
@@ -95,6 +97,11 @@ class DeftDataParallel:
         self.world = dist.get_world_size(process_group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(process_group) if dist.is_initialized() else 0
         self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.placement = self.cfg.update_placement
+        if self.placement == "auto":
+            self.placement = "end" if self.world == 1 else "start"
+        if self.placement not in ("end", "start", "bucket"):
+            raise DeftError(f"unknown update placement {self.placement!r}")
         if self.device.type != "cuda":
             raise DeftError("DeftDataParallel runs on CUDA devices only (no CPU fallback)")
         # DDP order: output-side parameter first (bucket 1 finishes backward first)
@@ -334,10 +341,10 @@ class DeftDataParallel:
         self._gather_slot = None
         self.scheduler = DeftScheduler(part, cluster, mult)
         self.capacity_multiplier = mult
-        blocks = self.cfg.update_blocks or (24 if self.cfg.update_placement == "start" else 0)
+        blocks = self.cfg.update_blocks or (16 if self.placement == "start" else 0)
         self.comm.set_update_blocks(blocks)
         self.planner = ExecutionPlanner(self.scheduler, self.cfg.n_slots, self.cfg.lookahead,
-                                        lag=2 if self.cfg.update_placement == "start" else 1)
+                                        lag=2 if self.placement == "start" else 1)
         self.link_streams = [torch.cuda.Stream(self.device) for _ in cluster.links]
         # runtime state
         self._slot_free = [None] * self.cfg.n_slots   # event: slot reusable (async mode)
@@ -359,7 +366,7 @@ class DeftDataParallel:
         self._hooks = [p.register_post_accumulate_grad_hook(self._on_grad)
                        for p in self.params]
         self._fwd_wait = {}
-        if self.cfg.update_placement == "start":
+        if self.placement == "start":
             self._install_forward_waits()
         return part
 
@@ -523,7 +530,7 @@ class DeftDataParallel:
         ev.record(torch.cuda.current_stream(self.device))
         for link, slot in self._fresh_now.pop(bidx, ()):
             self._issue_rs(link, slot, bidx, ev)
-        if self.cfg.update_placement == "bucket":
+        if self.placement == "bucket":
             for slot, k in self._due_now:
                 self._issue_update(slot, k, bidx, ev)
         self._fired[bidx] = True
@@ -535,7 +542,7 @@ class DeftDataParallel:
         self._touched = {}      # side streams forked from `comp` in this iteration
         if not self._sequential and self._version_ready is not None:
             comp.wait_event(self._version_ready)   # theta^(t) complete
-        if self.cfg.update_placement == "start" and it.due:
+        if self.placement == "start" and it.due:
             self._updates_at_start(comp, it.due)
         ev_fwd = torch.cuda.Event()
         ev_fwd.record(comp)
@@ -543,7 +550,7 @@ class DeftDataParallel:
             self._issue_rs(link, slot, bidx, ev_fwd)
         with self._autocast():
             loss = loss_fn(self.module, batch)
-        if self.cfg.update_placement == "start":
+        if self.placement == "start":
             for ev in self._fwd_wait.values():   # buckets no forward module touched
                 comp.wait_event(ev)
             self._fwd_wait = {}
@@ -565,7 +572,7 @@ class DeftDataParallel:
         for link, slot, bidx in it.bwd:
             self._issue_rs(link, slot, bidx, ev_bwd)
         self._fresh_now = dict(it.fresh)
-        self._due_now = it.due if self.cfg.update_placement != "start" else ()
+        self._due_now = it.due if self.placement != "start" else ()
         self._pending = list(self._bucket_nparams)
         self._fired = [False] * len(self.buckets)
         self._in_step = True
@@ -576,7 +583,7 @@ class DeftDataParallel:
         for b in range(len(self.buckets)):      # buckets whose params got no gradient
             if not self._fired[b]:
                 self._bucket_ready(b)
-        if self.cfg.update_placement == "end" and self._due_now:
+        if self.placement == "end" and self._due_now:
             self._updates_at_end(comp)
         if self._fresh_now:
             raise InternalInvariantError("fresh transfers left unreleased")
@@ -713,7 +720,7 @@ class DeftDataParallel:
         applied here (they would otherwise run at the start of iteration t); groups
         still in flight stay unapplied, as in the reference where unaccounted
         iterations are still in flight."""
-        if self.cfg.update_placement == "start" and hasattr(self, "planner"):
+        if self.placement == "start" and hasattr(self, "planner"):
             due, freed = self.planner.take_pending()
             if due:
                 caller = torch.cuda.current_stream(self.device)
