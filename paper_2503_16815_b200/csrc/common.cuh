@@ -92,7 +92,7 @@ cudaError_t launch_update_allgather_multi(const PeerPtrs& P, int rank, int world
 struct SchedArgs {
   int32_t n, L, T;
   const int64_t* comm;     // [n+1], by bucket id (index 0 unused)
-  const int64_t* bwd;      // [n+1] backward_us (only needed for the level caps)
+  const int64_t* bwd;      // [n+1] backward_us (level caps; exact mode never needs them)
   const int64_t* fcaps;    // [instances][L] forward-stage link capacities
   const int64_t* bcaps;    // [instances][L] backward-stage link capacities
   uint32_t* rows;          // [instances][(n+1) * words]

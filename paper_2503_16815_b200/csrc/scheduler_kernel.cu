@@ -32,10 +32,10 @@ constexpr int kSchedMaxN = 1024;
 constexpr int kSchedMaxLinks = 4;
 
 
-// record header: stage(0 fwd / 1 bwd), case(1..4), n_transfers, n_events,
-// merged(0/1), grad_group, grad_merge(0/1); then n_transfers x (link, id,
-// group, fresh) and n_events x (uid, first_origin, merge_count).
-constexpr int kHdr = 7;
+// Record layout, per stage: header of 7 ints -- stage (0 fwd / 1 bwd), case
+// (1..4), n_transfers, n_events, merged (0/1), grad_group, grad_merge (0/1) --
+// then n_transfers x (link, id, group, fresh) and n_events x (uid,
+// first_origin, merge_count).  Decoded by gpu_scheduler.py.
 
 struct SchedState {
   uint8_t in_cur[kSchedMaxN + 1];

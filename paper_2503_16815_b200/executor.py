@@ -79,10 +79,12 @@ class DeftConfig:
 
 
 class _Bucket:
-    __slots__ = ("id", "lo", "hi", "params")
+    """Bucket `id` owns elements [lo, hi) of the flat parameter / gradient buffers."""
+
+    __slots__ = ("id", "lo", "hi")
 
     def __init__(self, bid, lo, hi):
-        self.id, self.lo, self.hi, self.params = bid, lo, hi, []
+        self.id, self.lo, self.hi = bid, lo, hi
 
 
 class DeftDataParallel:
