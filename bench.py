@@ -375,6 +375,15 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
     return out
 
 
+def ncu_traffic(kernel, model, world):
+    """DRAM bytes per launch of `kernel` for this model / world size from a committed
+    ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    return json.loads(p.read_text()).get(f"{kernel}:{model}:w{world}")
+
+
 def _native_channel(name):
     from paper_2503_16815_b200 import _native
     return _native.CHANNEL_SM if name == "sm" else _native.CHANNEL_CE
@@ -608,11 +617,16 @@ def main():
     upd_name = "sgd_local_kernel" if world == 1 else (
         "update_allgather_multi_kernel" if ddp.placement == "end"
         else "update_allgather_kernel")
+    traffic = ncu_traffic(upd_name if kind == "update" else "reduce_scatter_kernel",
+                          args.model, world)
     roof = {"kernel": {"update": upd_name,
                        "reduce_scatter": "reduce_scatter_kernel"}[kind],
             "bound": "hbm" if hbm_bound else "nvlink",
             "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": None,
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "traffic_src": "profiles/ncu_traffic.json (dram__bytes_read.sum + "
+                           "dram__bytes_write.sum of one ncu --set full capture, per launch)"
+            if traffic else None,
             "measured": "isolated over this model's buckets, CUDA events, max over ranks",
             "in_step_achieved": round(in_step, 1) if in_step else None,
             "in_step_note": "same kernel inside the training step (overlapping backward "
