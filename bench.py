@@ -656,7 +656,9 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            # arithmetic of the DeFT path itself: gradient reduce + SGD/momentum update
+            "dtype": "bf16" if ddp.cfg.grad_dtype == torch.bfloat16 else "f32",
             "data": "synthetic (random-init weights, randn images / random tokens)",
             "config": {"workload": f"{args.model} DeFT delayed-update DP, batch "
                                    f"{args.batch}/GPU" + (", 224x224" if args.model != "gpt2"

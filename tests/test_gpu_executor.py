@@ -149,3 +149,33 @@ def test_multi_gpu_bf16_matches_oracle(placement):
             # the owner's fp32 master shard follows the oracle within 1e-6
             assert S.rel_err(theta[lo:hi], want[lo:hi]) <= S.TOL, (r, b)
             assert torch.equal(params[lo:hi], theta[lo:hi].bfloat16())
+
+
+class _ProbeWithUnused(S.Probe):
+    """One parameter never takes part in the loss: its gradient is None every
+    iteration, and the executor must treat its bucket range as a zero gradient."""
+
+    def forward(self, xs):
+        return sum((p * x).sum() for i, (p, x) in enumerate(zip(self.ps, xs)) if i != 3)
+
+
+@pytest.mark.parametrize("graphs", [True, False])
+def test_unused_parameter_gets_zero_gradient(graphs, monkeypatch):
+    monkeypatch.setattr(S, "Probe", _ProbeWithUnused)
+    iters = 10
+    theta, theta0, decisions = S.run_executor(1, 0, iters, cuda_graphs=graphs)
+    sizes = S.probe_sizes()
+    order = list(range(len(sizes)))[::-1]            # executor flat order
+    offs, o = {}, 0
+    for i in order:
+        offs[i] = (o, o + sizes[i])
+        o += sizes[i]
+    lo, hi = offs[3]
+
+    def grad(total, r, t):
+        g = S.flat_grad(total, r, t)
+        g[lo:hi] = 0
+        return g
+    want = S.oracle_theta(theta0, decisions, 1, iters, grad_fn=grad)
+    assert S.rel_err(theta, want) <= S.TOL
+    assert torch.equal(theta[lo:hi], theta0[lo:hi])   # zero grads, zero momentum: unchanged
