@@ -93,6 +93,17 @@ deft_status_t deft_solver_schedule(deft_solver* s, int32_t instances, int32_t n,
                                    const int64_t* bwd, const int64_t* fwd_caps,
                                    const int64_t* bwd_caps, int32_t* out, int64_t out_stride,
                                    int64_t* used, int32_t* status);
+/* The same in chunks, for unbounded runs: iterations [t0, t0+iterations), each
+ * instance starting from carry_in[i] (NULL = fresh scheduler) and leaving its
+ * state in carry_out[i] (NULL = not needed); carry records are
+ * deft_sched_carry_bytes() each, opaque to the caller. */
+size_t deft_sched_carry_bytes(void);
+deft_status_t deft_solver_schedule_chunk(deft_solver* s, int32_t instances, int32_t n,
+                                         int32_t n_links, int32_t t0, int32_t iterations,
+                                         const int64_t* comm, const int64_t* bwd,
+                                         const int64_t* fwd_caps, const int64_t* bwd_caps,
+                                         const void* carry_in, void* carry_out, int32_t* out,
+                                         int64_t out_stride, int64_t* used, int32_t* status);
 /* Device time (ms) of the kernels of the last solve, measured with CUDA events. */
 float deft_solver_last_kernel_ms(const deft_solver* s);
 

@@ -21,7 +21,8 @@ EXPORTED = (
     "deft_abi_version", "deft_last_error", "deft_launch_count",
     "deft_subset_sum_workspace_bytes", "deft_subset_sum_batched",
     "deft_solver_create", "deft_solver_destroy", "deft_solver_solve",
-    "deft_solver_last_kernel_ms", "deft_solver_schedule",
+    "deft_solver_last_kernel_ms", "deft_solver_schedule", "deft_solver_schedule_chunk",
+    "deft_sched_carry_bytes",
     "deft_mem_alloc", "deft_mem_free", "deft_mem_open", "deft_mem_close",
     "deft_comm_flag_bytes", "deft_comm_create", "deft_comm_destroy",
     "deft_comm_set_update_blocks",
@@ -55,6 +56,10 @@ def _declare(lib):
         "deft_solver_solve": (c_i32, [c_vp, c_i32, P(c_i32), P(c_i64), P(c_i64),
                                       P(ctypes.c_uint8), P(c_i64)]),
         "deft_solver_last_kernel_ms": (c_f32, [c_vp]),
+        "deft_sched_carry_bytes": (c_sz, []),
+        "deft_solver_schedule_chunk": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, c_i32,
+                                               P(c_i64), P(c_i64), P(c_i64), P(c_i64), c_vp,
+                                               c_vp, P(c_i32), c_i64, P(c_i64), P(c_i32)]),
         "deft_solver_schedule": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, P(c_i64), P(c_i64),
                                          P(c_i64), P(c_i64), P(c_i32), c_i64, P(c_i64),
                                          P(c_i32)]),

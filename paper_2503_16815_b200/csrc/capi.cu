@@ -526,13 +526,13 @@ extern "C" deft_status_t deft_bucket_update_multi(deft_comm* c, int32_t slot, in
 // ============================================================================
 // K5: persistent DeFT state machine (scheduler_kernel.cu)
 // ============================================================================
-extern "C" deft_status_t deft_solver_schedule(deft_solver* s, int32_t instances, int32_t n,
-                                              int32_t n_links, int32_t iterations,
-                                              const int64_t* comm, const int64_t* bwd,
-                                              const int64_t* fwd_caps,
-                                              const int64_t* bwd_caps, int32_t* out,
-                                              int64_t out_stride, int64_t* used,
-                                              int32_t* status) {
+extern "C" size_t deft_sched_carry_bytes(void) { return sizeof(SchedCarry); }
+
+extern "C" deft_status_t deft_solver_schedule_chunk(
+    deft_solver* s, int32_t instances, int32_t n, int32_t n_links, int32_t t0,
+    int32_t iterations, const int64_t* comm, const int64_t* bwd, const int64_t* fwd_caps,
+    const int64_t* bwd_caps, const void* carry_in, void* carry_out, int32_t* out,
+    int64_t out_stride, int64_t* used, int32_t* status) {
   if (!s || instances <= 0 || n <= 0 || n_links <= 0 || iterations < 0)
     return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_solver_schedule: bad arguments");
   if (cudaSetDevice(s->device) != cudaSuccess) return fail(DEFT_ERR_CUDA, "cudaSetDevice");
@@ -552,9 +552,10 @@ extern "C" deft_status_t deft_solver_schedule(deft_solver* s, int32_t instances,
   const size_t b_out = align_up((size_t)instances * out_stride * 4, 256);
   const size_t b_rows = align_up((size_t)instances * (n + 1) * words * 4, 256);
   const size_t b_reach = align_up((size_t)instances * (n + 1) * 4, 256);
-  const size_t in_bytes = 2 * b_vec + 2 * b_caps + b_stat;
-  const size_t dev_bytes = in_bytes + b_used + b_out + b_rows + b_reach;
-  deft_status_t st = grow(s, in_bytes + b_used + b_out, dev_bytes);
+  const size_t b_carry = align_up((size_t)instances * sizeof(SchedCarry), 256);
+  const size_t in_bytes = 2 * b_vec + 2 * b_caps + b_stat + b_carry;
+  const size_t dev_bytes = in_bytes + b_used + b_out + b_rows + b_reach + b_carry;
+  deft_status_t st = grow(s, in_bytes + b_used + b_out + b_carry, dev_bytes);
   if (st != DEFT_OK) return st;
   char* h = s->pinned;
   int64_t* hc = reinterpret_cast<int64_t*>(h);
@@ -565,6 +566,8 @@ extern "C" deft_status_t deft_solver_schedule(deft_solver* s, int32_t instances,
   memcpy(h + 2 * b_vec, fwd_caps, (size_t)instances * n_links * 8);
   memcpy(h + 2 * b_vec + b_caps, bwd_caps, (size_t)instances * n_links * 8);
   memset(h + 2 * b_vec + 2 * b_caps, 0, (size_t)instances * 4);
+  if (carry_in)
+    memcpy(h + 2 * b_vec + 2 * b_caps + b_stat, carry_in, (size_t)instances * sizeof(SchedCarry));
   char* d = s->dev;
   DEFT_CUDA(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, s->stream));
   SchedArgs A{};
@@ -583,6 +586,12 @@ extern "C" deft_status_t deft_solver_schedule(deft_solver* s, int32_t instances,
   A.words = words;
   A.reach = reinterpret_cast<int32_t*>(d + in_bytes + b_used + b_out + b_rows);
   A.smem_row_words = smem_words;
+  A.t0 = t0;
+  A.carry_in = carry_in ? reinterpret_cast<const SchedCarry*>(d + 2 * b_vec + 2 * b_caps + b_stat)
+                        : nullptr;
+  SchedCarry* d_carry_out =
+      reinterpret_cast<SchedCarry*>(d + in_bytes + b_used + b_out + b_rows + b_reach);
+  A.carry_out = carry_out ? d_carry_out : nullptr;
   DEFT_CUDA(cudaEventRecord(s->ev0, s->stream));
   cudaError_t e = launch_scheduler(A, instances, sched_smem_bytes(smem_words), s->stream);
   if (e != cudaSuccess) return cuda_fail(e, "deft_scheduler_kernel");
@@ -592,7 +601,12 @@ extern "C" deft_status_t deft_solver_schedule(deft_solver* s, int32_t instances,
   DEFT_CUDA(cudaMemcpyAsync(h + 2 * b_vec + 2 * b_caps, A.status, (size_t)instances * 4,
                             cudaMemcpyDeviceToHost, s->stream));
   DEFT_CUDA(cudaMemcpyAsync(h_out, A.used, b_used + b_out, cudaMemcpyDeviceToHost, s->stream));
+  char* h_carry = h_out + b_used + b_out;
+  if (carry_out)
+    DEFT_CUDA(cudaMemcpyAsync(h_carry, d_carry_out, (size_t)instances * sizeof(SchedCarry),
+                              cudaMemcpyDeviceToHost, s->stream));
   DEFT_CUDA(cudaStreamSynchronize(s->stream));
+  if (carry_out) memcpy(carry_out, h_carry, (size_t)instances * sizeof(SchedCarry));
   cudaEventElapsedTime(&s->last_ms, s->ev0, s->ev1);
   memcpy(status, h + 2 * b_vec + 2 * b_caps, (size_t)instances * 4);
   memcpy(used, h_out, (size_t)instances * 8);
@@ -602,4 +616,15 @@ extern "C" deft_status_t deft_solver_schedule(deft_solver* s, int32_t instances,
            (size_t)u * 4);
   }
   return DEFT_OK;
+}
+
+extern "C" deft_status_t deft_solver_schedule(deft_solver* s, int32_t instances, int32_t n,
+                                              int32_t n_links, int32_t iterations,
+                                              const int64_t* comm, const int64_t* bwd,
+                                              const int64_t* fwd_caps,
+                                              const int64_t* bwd_caps, int32_t* out,
+                                              int64_t out_stride, int64_t* used,
+                                              int32_t* status) {
+  return deft_solver_schedule_chunk(s, instances, n, n_links, 0, iterations, comm, bwd, fwd_caps,
+                                    bwd_caps, nullptr, nullptr, out, out_stride, used, status);
 }

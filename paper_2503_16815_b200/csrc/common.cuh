@@ -89,6 +89,15 @@ cudaError_t launch_update_allgather_multi(const PeerPtrs& P, int rank, int world
                                           const int64_t* offsets, const int64_t* numels,
                                           float lr, float momentum, float grad_scale,
                                           float* mom, int max_blocks, cudaStream_t stream);
+// State a scheduler instance carries from one chunk of iterations to the next
+// (pending updates are always flushed at the end of a backward stage).
+struct SchedCarry {
+  int32_t cur_uid, cur_first, cur_k, cur_count;
+  int64_t cur_backlog;
+  int32_t fut_uid, fut_first, fut_k, next_uid;
+  uint8_t in_cur[1032];  // by bucket id, n <= 1024
+};
+
 struct SchedArgs {
   int32_t n, L, T;
   const int64_t* comm;     // [n+1], by bucket id (index 0 unused)
@@ -103,6 +112,9 @@ struct SchedArgs {
   int32_t* status;         // [instances]
   int64_t* used;           // [instances] ints written to `out`
   int64_t smem_row_words;  // row words the launch's dynamic shared memory can hold
+  int32_t t0;              // iteration index of the first iteration of this chunk
+  const SchedCarry* carry_in;  // [instances] or null (fresh schedulers)
+  SchedCarry* carry_out;       // [instances] or null
 };
 int64_t sched_smem_bytes(int64_t words);
 cudaError_t launch_scheduler(const SchedArgs& a, int32_t instances, int64_t smem,

@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(kSchedThreads, 1) deft_scheduler_kernel(SchedA
     }
     st->rank_all[rank] = (int16_t)(i + 1);
   }
-  for (int i = tid; i <= n; i += kSchedThreads) st->in_cur[i] = 0;
+  for (int i = tid; i <= n; i += kSchedThreads)
+    st->in_cur[i] = a.carry_in ? a.carry_in[inst].in_cur[i] : 0;
   __syncthreads();
   if (tid >= 32) return;
 
@@ -167,12 +168,15 @@ __global__ void __launch_bounds__(kSchedThreads, 1) deft_scheduler_kernel(SchedA
   int32_t* out = a.out + (int64_t)inst * a.out_stride;
   int64_t pos = 0;
   bool overflow = false;
-  int next_uid = 0;
+  const SchedCarry* cin = a.carry_in ? a.carry_in + inst : nullptr;
+  int next_uid = cin ? cin->next_uid : 0;
   // current group (leftovers being sent): exists iff some in_cur flag is set
-  int cur_uid = -1, cur_first = 0, cur_k = 0, cur_count = 0;
-  int64_t cur_backlog = 0;
+  int cur_uid = cin ? cin->cur_uid : -1, cur_first = cin ? cin->cur_first : 0;
+  int cur_k = cin ? cin->cur_k : 0, cur_count = cin ? cin->cur_count : 0;
+  int64_t cur_backlog = cin ? cin->cur_backlog : 0;
   // future group (all buckets, stored / merged, not yet started)
-  int fut_uid = -1, fut_first = 0, fut_k = 0;
+  int fut_uid = cin ? cin->fut_uid : -1, fut_first = cin ? cin->fut_first : 0;
+  int fut_k = cin ? cin->fut_k : 0;
   // pending update events (drained groups) -- at most two per stage
   int pend_n = 0, pend_uid[4], pend_first[4], pend_k[4];
 
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) deft_scheduler_kernel(SchedA
     return 0;
   };
 
-  for (int t = 0; t < a.T && !overflow; ++t) {
+  for (int t = a.t0; t < a.t0 + a.T && !overflow; ++t) {
     // ------------------------------ forward stage: Case 1
     if (lane == 0) {
       st->n_tr = 0;
@@ -412,6 +416,14 @@ __global__ void __launch_bounds__(kSchedThreads, 1) deft_scheduler_kernel(SchedA
   if (lane == 0) {
     if (a.status[inst] == 0 && overflow) a.status[inst] = -3;
     a.used[inst] = pos;
+    if (a.carry_out) {
+      SchedCarry* c = a.carry_out + inst;
+      c->cur_uid = cur_uid; c->cur_first = cur_first; c->cur_k = cur_k;
+      c->cur_count = cur_count; c->cur_backlog = cur_backlog;
+      c->fut_uid = fut_uid; c->fut_first = fut_first; c->fut_k = fut_k;
+      c->next_uid = next_uid;
+      for (int i = 0; i <= n; ++i) c->in_cur[i] = st->in_cur[i];
+    }
   }
 }
 

@@ -59,6 +59,7 @@ class DeftConfig:
     walk: WalkParams | None = None          # run the feedback loop when given
     capacity_multiplier: float = 1.0
     lookahead: int = 32                     # decisions generated ahead of execution
+    schedule_engine: str = "auto"           # "kernel" (K5 chunks), "host", "auto"
     use_ce_channel: bool = True             # second link = copy engines
     instrument: bool = False                # CUDA events around every native launch
     # capture + replay each distinct iteration shape; "auto" = keep graphs only if
@@ -341,7 +342,13 @@ class DeftDataParallel:
                 self._bucket_nparams[b] += 1
                 self._bucket_params[b].append(i)
         self._gather_slot = None
-        self.scheduler = DeftScheduler(part, cluster, mult)
+        from .gpu_scheduler import KernelScheduler
+        from .scheduler import use_kernel_engine
+        if (use_kernel_engine(self.cfg.schedule_engine)
+                and KernelScheduler.supported(part, cluster, mult)):
+            self.scheduler = KernelScheduler(part, cluster, mult)   # K5, in chunks
+        else:
+            self.scheduler = DeftScheduler(part, cluster, mult)
         self.capacity_multiplier = mult
         blocks = self.cfg.update_blocks or (16 if self.placement == "start" else 0)
         self.comm.set_update_blocks(blocks)

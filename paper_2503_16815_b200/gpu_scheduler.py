@@ -27,12 +27,12 @@ _CASES = {1: Case.CASE1, 2: Case.CASE2, 3: Case.CASE3, 4: Case.CASE4}
 
 
 def _decode(rec: np.ndarray, n_used: int, names: list[str], all_ids: tuple[int, ...],
-            iterations: int) -> list[ScheduleDecision]:
+            iterations: int, t0: int = 0) -> list[ScheduleDecision]:
     out: list[ScheduleDecision] = []
     r = rec[:n_used].tolist()
     pos = 0
     L = len(names)
-    for t in range(iterations):
+    for t in range(t0, t0 + iterations):
         for expect_stage in (0, 1):
             stage, cas, n_tr, n_ev, merged, grad_uid, grad_merge = r[pos:pos + _HDR]
             pos += _HDR
@@ -150,4 +150,75 @@ def run_schedules_lazy(profile: ModelProfile, cluster: ClusterSpec, multipliers:
     return res
 
 
-__all__ = ["run_schedules", "run_schedules_lazy", "KernelSchedule"]
+class KernelScheduler:
+    """``DeftScheduler``'s stage API (schedule_forward / schedule_backward, called in
+    order) backed by K5: the decisions are produced on the GPU `chunk` iterations
+    at a time, the scheduler state carried between chunks inside the kernel's
+    carry records.  Used by the executor for unbounded training runs."""
+
+    def __init__(self, profile: ModelProfile, cluster: ClusterSpec,
+                 capacity_multiplier: float = 1.0, chunk: int = 256):
+        self.profile, self.cluster, self.chunk = profile, cluster, chunk
+        cm = CapacityModel.from_profile(profile, cluster, capacity_multiplier)
+        self._fcaps = np.array(cm.stage_capacities("forward"), dtype=np.int64)
+        self._bcaps = np.array(cm.stage_capacities("backward"), dtype=np.int64)
+        self._comm = np.array([b.comm_fast_us for b in profile.buckets], dtype=np.int64)
+        self._bwd = np.array([b.backward_us for b in profile.buckets], dtype=np.int64)
+        self._names = [l.name for l in cluster.links]
+        self._ids = tuple(b.id for b in profile.buckets)
+        self._carry = None
+        self._next_t = 0
+        self._ready: dict[tuple[int, str], ScheduleDecision] = {}
+        self.chunks = 0
+
+    @staticmethod
+    def supported(profile: ModelProfile, cluster: ClusterSpec, mult: float = 1.0) -> bool:
+        cm = CapacityModel.from_profile(profile, cluster, mult)
+        return (sum(cm.stage_capacities("backward")) <= 10_000_000 and profile.n_buckets <= 1024
+                and len(cluster.links) <= 4)
+
+    def _fetch(self):
+        solver = _native.subset_sum_solver()
+        n, L, T, t0 = len(self._ids), len(self._names), self.chunk, self._next_t
+        stride = T * 2 * (_HDR + 8 * n + 12) + 16
+        out = np.zeros(stride, dtype=np.int32)
+        used = np.zeros(1, dtype=np.int64)
+        status = np.zeros(1, dtype=np.int32)
+        cbytes = int(_native.lib().deft_sched_carry_bytes())
+        carry_out = np.zeros(cbytes, dtype=np.uint8)
+        cin = None if self._carry is None else self._carry.ctypes.data_as(_native.c_vp)
+        st = _native.lib().deft_solver_schedule_chunk(
+            solver._h, 1, n, L, t0, T, self._comm.ctypes.data_as(P(c_i64)),
+            self._bwd.ctypes.data_as(P(c_i64)), self._fcaps.ctypes.data_as(P(c_i64)),
+            self._bcaps.ctypes.data_as(P(c_i64)), cin, carry_out.ctypes.data_as(_native.c_vp),
+            out.ctypes.data_as(P(c_i32)), stride, used.ctypes.data_as(P(c_i64)),
+            status.ctypes.data_as(P(c_i32)))
+        _native.check(st, "deft_solver_schedule_chunk")
+        if status[0] != 0:
+            raise InternalInvariantError(f"scheduler kernel status {status[0]}")
+        for d in _decode(out, int(used[0]), self._names, self._ids, T, t0):
+            self._ready[(d.iteration, d.stage)] = d
+        self._carry = carry_out
+        self._next_t += T
+        self.chunks += 1
+
+    def _take(self, iteration: int, stage: str) -> ScheduleDecision:
+        while iteration >= self._next_t:
+            self._fetch()
+        return self._ready.pop((iteration, stage))
+
+    def schedule_forward(self, iteration: int) -> ScheduleDecision:
+        return self._take(iteration, "forward")
+
+    def schedule_backward(self, iteration: int) -> ScheduleDecision:
+        return self._take(iteration, "backward")
+
+    def run(self, iterations: int) -> list[ScheduleDecision]:
+        out = []
+        for k in range(iterations):
+            out.append(self.schedule_forward(k))
+            out.append(self.schedule_backward(k))
+        return out
+
+
+__all__ = ["run_schedules", "run_schedules_lazy", "KernelSchedule", "KernelScheduler"]

@@ -156,3 +156,29 @@ def test_feedback_loop_kernel_engine(golden_index, golden_inputs):
             assert hashlib.sha256(text.encode()).hexdigest() == v["final_sha256"], e["key"]
             assert (got.preserved, got.retries, got.ratio) == \
                 (v["preserved"], v["retries"], v["ratio"])
+
+
+@pytest.mark.parametrize("chunk", [1, 7, 64])
+def test_kernel_scheduler_chunks_match_host(golden_index, golden_inputs, chunk):
+    """K5 in chunks with carried state == the host state machine, across chunk
+    boundaries that fall inside merged groups."""
+    from test_host_logic import build_product_inputs
+    from paper_2503_16815_b200.gpu_scheduler import KernelScheduler
+    keys = ("uniform48__equal_dual__raw", "uniform36__equal_dual__raw__m1",
+            "vgg19__dual__bw0.25", "gpt2__fast__bw0.25", "resnet101__fast__bw0.25",
+            "measured_vgg19_w4__x200")
+    n = 0
+    for e in golden_index:
+        if e["key"] not in keys:
+            continue
+        prof, cluster, cfg, mult, _ = build_product_inputs(e, golden_inputs)
+        part = D.partition_buckets(prof, cfg) if cfg is not None else prof
+        if not KernelScheduler.supported(part, cluster, mult):
+            continue
+        iters = 70
+        got = KernelScheduler(part, cluster, mult, chunk=chunk).run(iters)
+        want = D.DeftScheduler(part, cluster, mult).run(iters)
+        for a, b in zip(got, want):
+            assert a == b and a.exec == b.exec, (e["key"], chunk, a.iteration, a.stage)
+        n += 1
+    assert n >= 5
