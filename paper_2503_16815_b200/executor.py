@@ -364,6 +364,7 @@ class DeftDataParallel:
         # join the compute stream at the end of each iteration)
         self._sequential = bool(self.cfg.cuda_graphs)
         self._use_graphs = bool(self.cfg.cuda_graphs)
+        self._freeze_graphs = False
         self.graph_choice = None
         self._graphs: dict = {}
         self._seen: dict = {}
@@ -661,6 +662,14 @@ class DeftDataParallel:
             streak = streak + 1 if self.last_step_kind == "replay" else 0
             if not self._use_graphs:
                 streak = steady
+        if self._use_graphs and streak < steady:
+            # the iteration shapes never settled (e.g. irregular merge patterns):
+            # capturing on the fly would keep paying for captures -- run eagerly
+            self._use_graphs = False
+            self.graph_choice = {"use_graphs": False, "reason": "no steady-state shape"}
+            return n
+        # from now on unseen iteration shapes run eagerly instead of being captured
+        self._freeze_graphs = True
         if self.cfg.cuda_graphs == "auto" and self._use_graphs and compare > 0:
             t_graph = self._time_steps(batch, loss_fn, compare)
             self._use_graphs = False
@@ -707,7 +716,7 @@ class DeftDataParallel:
             return loss
         seen = self._seen.get(it.key, 0)
         self._seen[it.key] = seen + 1
-        if seen < self.cfg.graph_warmup:
+        if seen < self.cfg.graph_warmup or self._freeze_graphs:
             self.last_step_kind = "eager"
             return self._run_iteration(it, static, loss_fn)
         self.compute_stream.synchronize()
