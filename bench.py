@@ -338,7 +338,11 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
             t = torch.tensor([ms], device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        n = 1 if (kind == "update" and ddp.placement == "end") else len(ddp.buckets)
+        n = len(ddp.buckets)
+        if kind == "update" and ddp.placement == "end":
+            n = 1
+        elif kind == "update" and ddp.placement == "start":
+            n = len(ddp._start_groups())
         out[kind] = {"launches": n, "ms_per_pass": round(ms, 4),
                      "avg_launch_us": round(ms / n * 1e3, 2), "bytes_per_pass": nbytes,
                      "achieved_gbs": round(nbytes / (ms / 1e3) / 1e9, 1)}
@@ -352,13 +356,17 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
     else:               # NVLink bytes: updated params stored to the W-1 peers
         upd_bytes = sum((b.hi - b.lo) * esz * (world - 1) // world for b in ddp.buckets)
 
-    def updates():
-        if ddp.placement == "end":   # the step's own launch shape
+    def updates():   # the step's own launch shape
+        if ddp.placement == "end":
             ddp.comm.update_multi(slot, [(b.lo, b.hi) for b in ddp.buckets], 1.0, 0.0, 0.9,
                                   ddp.mom, s)
-            return
-        for b in ddp.buckets:
-            ddp.comm.update(slot, b.lo, b.hi - b.lo, 0.0, 0.9, 1.0, ddp.mom, s)
+        elif ddp.placement == "start":
+            for g in ddp._start_groups():
+                ddp.comm.update_multi(slot, [(ddp.buckets[b].lo, ddp.buckets[b].hi) for b in g],
+                                      1.0, 0.0, 0.9, ddp.mom, s)
+        else:
+            for b in ddp.buckets:
+                ddp.comm.update(slot, b.lo, b.hi - b.lo, 0.0, 0.9, 1.0, ddp.mom, s)
     with torch.cuda.stream(s):
         run("update", updates, upd_bytes)
         if world > 1:
@@ -615,7 +623,7 @@ def main():
         in_step = (r["bytes"] / r["launches"]) / (avg_ms / 1e3) / 1e9
     achieved = iso[kind]["achieved_gbs"]
     upd_name = "sgd_local_kernel" if world == 1 else (
-        "update_allgather_multi_kernel" if ddp.placement == "end"
+        "update_allgather_multi_kernel" if ddp.placement in ("end", "start")
         else "update_allgather_kernel")
     traffic = ncu_traffic(upd_name if kind == "update" else "reduce_scatter_kernel",
                           args.model, world)

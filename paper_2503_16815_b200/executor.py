@@ -76,6 +76,7 @@ class DeftConfig:
     # "start" placement a small budget lets the update overlap the forward instead
     # of displacing it.
     update_blocks: int = 0
+    start_groups: int = 8                   # update launches per event with "start"
     graph_warmup: int = 1                   # eager runs of a shape before it is captured
 
 
@@ -472,19 +473,53 @@ class DeftDataParallel:
                 self._module_buckets[m] = bl
                 self._hooks.append(m.register_forward_pre_hook(pre))
 
+    def _start_groups(self) -> list[list[int]]:
+        """Consecutive buckets in forward order (input side first) coalesced into at
+        most `start_groups` groups of similar size: one update launch per group."""
+        if getattr(self, "_groups_cache", None) is None:
+            order = list(range(len(self.buckets) - 1, -1, -1))
+            n_groups = max(1, min(self.cfg.start_groups, len(order)))
+            target = self.total / n_groups
+            groups, cur, acc = [], [], 0
+            for b in order:
+                cur.append(b)
+                acc += self.buckets[b].hi - self.buckets[b].lo
+                if acc >= target * (len(groups) + 1) and len(groups) < n_groups - 1:
+                    groups.append(cur)
+                    cur = []
+            if cur:
+                groups.append(cur)
+            self._groups_cache = groups
+        return self._groups_cache
+
     def _updates_at_start(self, comp, due):
         """Updates of decision (t-2, backward) at the start of iteration t, input-side
-        bucket first, overlapping the forward: bucket b's forward waits only for b."""
+        buckets first, overlapping the forward: a bucket's forward waits only for its
+        own group's update launch."""
         ev0 = torch.cuda.Event()
         ev0.record(comp)
         s = self.update_stream
+        s.wait_event(ev0)
+        self._touched[id(s)] = s
         self._fwd_wait = {}
-        for bidx in range(len(self.buckets) - 1, -1, -1):   # forward order: bucket n first
+        esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
+        for group in self._start_groups():
+            ranges = [(self.buckets[b].lo, self.buckets[b].hi) for b in group]
+            elems = sum(hi - lo for lo, hi in ranges)
+            nbytes = elems * 20 if self.world == 1 else elems * esz * (self.world - 1) // self.world
             for slot, k in due:
-                self._issue_update(slot, k, bidx, ev0)
+                if self.world > 1:
+                    for b in group:          # the reduce-scatters of this group are done
+                        rs = self._rs_done.pop((slot, b), None)
+                        if rs is not None:
+                            s.wait_event(rs)
+                self._timed("update", s, lambda: self.comm.update_multi(
+                    slot, ranges, 1.0 / (self.world * k), self.cfg.lr, self.cfg.momentum,
+                    self.mom, s), nbytes)
             ev = torch.cuda.Event()
             ev.record(s)
-            self._fwd_wait[bidx] = ev
+            for b in group:
+                self._fwd_wait[b] = ev
 
     def _updates_at_end(self, comp):
         """All due updates after the whole backward (every no-read window is open):
