@@ -268,9 +268,15 @@ static void rs_dispatch(int world, int grid, cudaStream_t stream, const PeerPtrs
 #undef DEFT_RS_CASE
 }
 
+bool launch_reduce_scatter_tma(const PeerPtrs& P, int rank, int world, int dtype,
+                               int64_t slot_base, int64_t offset, int64_t numel,
+                               cudaStream_t stream);
+
 cudaError_t launch_reduce_scatter_sm(const PeerPtrs& P, int rank, int world, int dtype,
                                      int64_t slot_base, int64_t offset, int64_t numel,
                                      cudaStream_t stream) {
+  if (launch_reduce_scatter_tma(P, rank, world, dtype, slot_base, offset, numel, stream))
+    return cudaGetLastError();
   const int align = dtype == 0 ? 4 : 8;
   const ShardRange sh = shard_of(offset, numel, rank, world, align);
   const int grid = comm_grid_for((numel + world - 1) / world);
@@ -718,6 +724,192 @@ cudaError_t launch_update_allgather_multi(const PeerPtrs& P, int rank, int world
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+}  // namespace deft
+
+namespace deft {
+
+// ============================================================================
+// Reduce-scatter, SM channel, TMA-staged: per CTA a ring of kTmaStages shared-
+// memory stages; one elected thread issues one cp.async.bulk (global -> shared,
+// completing on the stage's mbarrier) per rank for the next chunk while all
+// threads sum the current chunk's W copies in fp32 and store the result.  The
+// bytes in flight are held by the copy engine of the SM (TMA), not by thread
+// registers, so a few CTAs saturate NVLink and the rest of the SMs stay with
+// the concurrent backward.
+// ============================================================================
+constexpr int kTmaThreads = 256;
+constexpr int kTmaStages = 4;
+constexpr int kTmaStageBytes = 32 * 1024;  // W peer chunks per stage
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst_smem)), "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename T, int W>
+__global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
+    PeerPtrs P, int rank, int64_t slot_base, int64_t lo, int64_t hi) {
+  using V = Vec<T>;
+  extern __shared__ __align__(128) unsigned char tma_smem[];
+  __shared__ __align__(8) uint64_t full[kTmaStages];
+  // elements per peer chunk: a stage holds W chunks, 16-byte granular
+  constexpr int64_t kChunk = (kTmaStageBytes / W / (int)sizeof(T)) / 8 * 8;
+  const uint32_t epoch = take_epochs(P, rank, kBarrierRS, 1u) + 1u;
+  peer_block_barrier(P, rank, W, kBarrierRS, blockIdx.x, epoch);
+  const T* src[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) src[k] = reinterpret_cast<const T*>(P.grads[k]) + slot_base;
+  T* dst = reinterpret_cast<T*>(P.grads[rank]) + slot_base;
+  const Span s = split_span<V::N>(lo, hi);
+  if (blockIdx.x == 0) {  // unaligned edges
+    for (int64_t e = s.head_lo + threadIdx.x; e < s.head_hi; e += blockDim.x) {
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < W; ++k) acc += V::scalar(src[k] + e);
+      V::put(dst + e, acc);
+    }
+    for (int64_t e = s.tail_lo + threadIdx.x; e < s.tail_hi; e += blockDim.x) {
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < W; ++k) acc += V::scalar(src[k] + e);
+      V::put(dst + e, acc);
+    }
+  }
+  // this CTA's contiguous share of the aligned body, in chunks
+  const int64_t body = s.body_hi - s.body_lo;
+  const int64_t n_chunks = (body + kChunk - 1) / kChunk;
+  const int64_t c_begin = n_chunks * blockIdx.x / gridDim.x;
+  const int64_t c_end = n_chunks * (blockIdx.x + 1) / gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kTmaStages; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto stage_ptr = [&](int st, int k) -> T* {
+    return reinterpret_cast<T*>(tma_smem + (size_t)st * kTmaStageBytes) + (int64_t)k * kChunk;
+  };
+  auto issue = [&](int64_t c) {  // one elected thread: W bulk copies of chunk c
+    const int st = (int)((c - c_begin) % kTmaStages);
+    const int64_t e0 = s.body_lo + c * kChunk;
+    const int64_t len = min(kChunk, s.body_hi - e0);
+    const uint32_t bytes = (uint32_t)(len * sizeof(T));
+    // the stage was last read through the generic proxy; order that before the
+    // async-proxy (TMA) writes that refill it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&full[st], bytes * W);
+#pragma unroll
+    for (int k = 0; k < W; ++k) tma_load_1d(stage_ptr(st, k), src[k] + e0, bytes, &full[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t c = c_begin; c < min(c_end, c_begin + kTmaStages - 1); ++c) issue(c);
+  for (int64_t c = c_begin; c < c_end; ++c) {
+    const int st = (int)((c - c_begin) % kTmaStages);
+    const uint32_t parity = (uint32_t)(((c - c_begin) / kTmaStages) & 1);
+    // keep the ring full: chunk c + S - 1 goes into the stage freed at the end of c - 1
+    if (threadIdx.x == 0 && c + kTmaStages - 1 < c_end) issue(c + kTmaStages - 1);
+    mbar_wait(&full[st], parity);
+    const int64_t e0 = s.body_lo + c * kChunk;
+    const int64_t len = min(kChunk, s.body_hi - e0);
+    using Raw = typename V::Raw;
+    for (int64_t v = threadIdx.x; v < len / V::N; v += blockDim.x) {
+      float acc[V::N], tmp[V::N];
+      V::to_f32(reinterpret_cast<const Raw*>(stage_ptr(st, 0))[v], acc);
+#pragma unroll
+      for (int k = 1; k < W; ++k) {
+        V::to_f32(reinterpret_cast<const Raw*>(stage_ptr(st, k))[v], tmp);
+#pragma unroll
+        for (int q = 0; q < V::N; ++q) acc[q] += tmp[q];
+      }
+      reinterpret_cast<Raw*>(dst + e0)[v] = V::from_f32(acc);
+    }
+    __syncthreads();  // stage st fully consumed before it is refilled
+  }
+}
+
+template <typename T>
+static void rs_tma_dispatch(int world, int grid, cudaStream_t stream, const PeerPtrs& P,
+                            int rank, int64_t slot_base, int64_t lo, int64_t hi) {
+  const size_t smem = (size_t)kTmaStages * kTmaStageBytes;
+#define DEFT_RST_CASE(WW)                                                                      \
+  case WW: {                                                                                   \
+    static bool attr = false;                                                                  \
+    if (!attr) {                                                                               \
+      cudaFuncSetAttribute(reduce_scatter_tma_kernel<T, WW>,                                   \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+      attr = true;                                                                             \
+    }                                                                                          \
+    reduce_scatter_tma_kernel<T, WW><<<grid, kTmaThreads, smem, stream>>>(P, rank, slot_base,  \
+                                                                          lo, hi);             \
+    break;                                                                                     \
+  }
+  switch (world) {
+    DEFT_RST_CASE(2) DEFT_RST_CASE(3) DEFT_RST_CASE(4) DEFT_RST_CASE(5)
+    DEFT_RST_CASE(6) DEFT_RST_CASE(7) DEFT_RST_CASE(8)
+    default: break;
+  }
+#undef DEFT_RST_CASE
+}
+
+// DEFT_RS_IMPL=tma|ldg selects the SM-channel reduce-scatter; DEFT_RS_TMA_BLOCKS
+// its CTA count (default 24).
+static int rs_impl_tma() {
+  static int v = [] {
+    const char* e = getenv("DEFT_RS_IMPL");
+    return e && e[0] == 't' ? 1 : 0;
+  }();
+  return v;
+}
+static int rs_tma_blocks() {
+  static int v = [] {
+    const char* e = getenv("DEFT_RS_TMA_BLOCKS");
+    int x = e ? atoi(e) : 24;
+    return x < 1 ? 1 : (x > kMaxCommBlocks ? kMaxCommBlocks : x);
+  }();
+  return v;
+}
+
+bool launch_reduce_scatter_tma(const PeerPtrs& P, int rank, int world, int dtype,
+                               int64_t slot_base, int64_t offset, int64_t numel,
+                               cudaStream_t stream) {
+  if (!rs_impl_tma()) return false;
+  const ShardRange sh = shard_of(offset, numel, rank, world, dtype == 0 ? 4 : 8);
+  const int64_t per = (numel + world - 1) / world;
+  int grid = (int)((per + 32767) / 32768);
+  if (grid < 1) grid = 1;
+  if (grid > rs_tma_blocks()) grid = rs_tma_blocks();
+  if (dtype == 0)
+    rs_tma_dispatch<float>(world, grid, stream, P, rank, slot_base, sh.lo, sh.hi);
+  else
+    rs_tma_dispatch<__nv_bfloat16>(world, grid, stream, P, rank, slot_base, sh.lo, sh.hi);
+  count_launch();
+  return true;
 }
 
 }  // namespace deft

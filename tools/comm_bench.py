@@ -48,6 +48,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes-mb", default="1,4,16,64,256")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--check", action="store_true",
+                    help="verify every reduce-scatter result before timing")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -65,6 +67,22 @@ def main():
         n = mb * 2**20 // 4
         nbytes = n * 4
         res = {"bucket_mb": mb, "world": W}
+        if args.check:
+            for ch in (_native.CHANNEL_SM, _native.CHANNEL_CE):
+                idx = torch.arange(n, device=dev, dtype=torch.float32)
+                comm.grads[0, :n].copy_(torch.sin(idx * 0.001 + rank))
+                torch.cuda.synchronize()
+                dist.barrier()
+                comm.reduce_scatter(ch, 0, 0, n, s)
+                torch.cuda.synchronize()
+                want = sum(torch.sin(idx * 0.001 + r) for r in range(W))
+                per = (n + W - 1) // W
+                lo = 0 if rank == 0 else -(-(rank * per) // 4) * 4
+                hi = n if rank == W - 1 else -(-((rank + 1) * per) // 4) * 4
+                err = float((comm.grads[0, lo:hi] - want[lo:hi]).abs().max())
+                res[f"check_err_ch{ch}"] = err
+                assert err < 1e-4, (ch, err)
+                dist.barrier()
         with torch.cuda.stream(s):
             res["rs_sm_ms"] = timeit(lambda: comm.reduce_scatter(_native.CHANNEL_SM, 0, 0, n, s),
                                      args.reps, 3, s, dev)
