@@ -877,12 +877,13 @@ static void rs_tma_dispatch(int world, int grid, cudaStream_t stream, const Peer
 #undef DEFT_RST_CASE
 }
 
-// DEFT_RS_IMPL=tma|ldg selects the SM-channel reduce-scatter; DEFT_RS_TMA_BLOCKS
-// its CTA count (default 24).
+// DEFT_RS_IMPL=tma|ldg selects the SM-channel reduce-scatter (default tma: the
+// same NVLink bandwidth from 24 CTAs as the LDG kernel from 128, K2b);
+// DEFT_RS_TMA_BLOCKS its CTA count (default 24).
 static int rs_impl_tma() {
   static int v = [] {
     const char* e = getenv("DEFT_RS_IMPL");
-    return e && e[0] == 't' ? 1 : 0;
+    return e && e[0] == 'l' ? 0 : 1;
   }();
   return v;
 }
