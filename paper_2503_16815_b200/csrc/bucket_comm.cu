@@ -679,11 +679,20 @@ __global__ void __launch_bounds__(kLocalThreads) update_allgather_multi_kernel(
   peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 2u);
 }
 
+bool launch_update_allgather_tma(const PeerPtrs& P, int rank, int world, int dtype,
+                                 int64_t slot_base, int32_t count, const int64_t* offsets,
+                                 const int64_t* numels, float lr, float momentum,
+                                 float grad_scale, float* mom, int max_blocks,
+                                 cudaStream_t stream);
+
 cudaError_t launch_update_allgather_multi(const PeerPtrs& P, int rank, int world, int dtype,
                                           int64_t slot_base, int32_t count,
                                           const int64_t* offsets, const int64_t* numels,
                                           float lr, float momentum, float grad_scale,
                                           float* mom, int max_blocks, cudaStream_t stream) {
+  if (launch_update_allgather_tma(P, rank, world, dtype, slot_base, count, offsets, numels, lr,
+                                  momentum, grad_scale, mom, max_blocks, stream))
+    return cudaGetLastError();
   const int align = dtype == 0 ? 4 : 8;
   for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
     SegTable t{};
@@ -910,6 +919,227 @@ bool launch_reduce_scatter_tma(const PeerPtrs& P, int rank, int world, int dtype
   else
     rs_tma_dispatch<__nv_bfloat16>(world, grid, stream, P, rank, slot_base, sh.lo, sh.hi);
   count_launch();
+  return true;
+}
+
+}  // namespace deft
+
+namespace deft {
+
+// ============================================================================
+// Multi-bucket fused update + all-gather, TMA-pipelined (W > 1).  Same math and
+// barriers as update_allgather_multi_kernel; per CTA a ring of shared-memory
+// stages: one elected thread bulk-loads a chunk of g / v / p (cp.async.bulk,
+// mbarrier complete_tx), all threads update it in place, and the elected
+// thread bulk-STORES the new momentum (and fp32 master) locally and the new
+// parameters to every rank (cp.async.bulk.global.shared::cta, peer addresses).
+// The bytes in flight live in the TMA unit, so the small CTA budget the
+// "start" placement uses still streams at NVLink rate.
+// ============================================================================
+constexpr int kUpdTmaThreads = 256;
+constexpr int kUpdTmaStages = 3;
+constexpr int kUpdChunk = 2048;  // elements per chunk (multiple of 8)
+
+__device__ __forceinline__ void tma_store_1d(void* dst_gmem, const void* src_smem,
+                                             uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst_gmem),
+               "r"(smem_u32(src_smem)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+struct ChunkTable {           // this rank's owned shards, cut into TMA chunks
+  int64_t off[kMaxSeg];       // aligned body start of each segment
+  int64_t len[kMaxSeg];       // aligned body length (multiple of 8 elements)
+  int64_t first[kMaxSeg + 1]; // prefix of chunks per segment
+  int64_t head_lo[kMaxSeg], head_hi[kMaxSeg], tail_lo[kMaxSeg], tail_hi[kMaxSeg];
+  int32_t count;
+};
+
+template <typename T, int W>
+__global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
+    PeerPtrs P, int rank, int64_t slot_base, ChunkTable t, float lr, float momentum,
+    float scale, float* __restrict__ mom) {
+  using V = Vec<T>;
+  constexpr bool kMaster = sizeof(T) == 2;
+  // stage layout: g (T) | v (f32) | p (f32) | p_out (T, bf16 only)
+  constexpr int64_t kG = (int64_t)kUpdChunk * sizeof(T);
+  constexpr int64_t kF = (int64_t)kUpdChunk * 4;
+  constexpr int64_t kStage = kG + 2 * kF + (kMaster ? kG : 0);
+  extern __shared__ __align__(128) unsigned char usmem[];
+  __shared__ __align__(8) uint64_t full[kUpdTmaStages];
+
+  const uint32_t epoch = take_epochs(P, rank, kBarrierUpdate, 2u);
+  peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 1u);
+  const T* g = reinterpret_cast<const T*>(P.grads[rank]) + slot_base;
+  float* ref = kMaster ? P.master : reinterpret_cast<float*>(P.params[rank]);
+  T* dst[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) dst[k] = reinterpret_cast<T*>(P.params[k]);
+
+  // unaligned edges of every segment: block 0, scalar
+  if (blockIdx.x == 0) {
+    for (int sgi = 0; sgi < t.count; ++sgi) {
+      for (int part = 0; part < 2; ++part) {
+        const int64_t a = part ? t.tail_lo[sgi] : t.head_lo[sgi];
+        const int64_t b = part ? t.tail_hi[sgi] : t.head_hi[sgi];
+        for (int64_t e = a + threadIdx.x; e < b; e += blockDim.x) {
+          const float v = fmaf(momentum, mom[e], V::scalar(g + e) * scale);
+          mom[e] = v;
+          const float p = fmaf(-lr, v, ref[e]);
+          if (kMaster) ref[e] = p;
+#pragma unroll
+          for (int k = 0; k < W; ++k) store1(dst[k] + e, p);
+        }
+      }
+    }
+  }
+  const int64_t n_chunks = t.first[t.count];
+  const int64_t c_begin = n_chunks * blockIdx.x / gridDim.x;
+  const int64_t c_end = n_chunks * (blockIdx.x + 1) / gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kUpdTmaStages; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto chunk_range = [&](int64_t c, int64_t* e0, int64_t* len) {
+    int sgi = 0;
+    while (c >= t.first[sgi + 1]) ++sgi;
+    const int64_t k = c - t.first[sgi];
+    *e0 = t.off[sgi] + k * kUpdChunk;
+    const int64_t rem = t.off[sgi] + t.len[sgi] - *e0;
+    *len = rem < kUpdChunk ? rem : kUpdChunk;
+  };
+  auto base = [&](int st) { return usmem + (size_t)st * kStage; };
+  auto issue_load = [&](int64_t c) {
+    const int st = (int)((c - c_begin) % kUpdTmaStages);
+    int64_t e0, len;
+    chunk_range(c, &e0, &len);
+    tma_store_wait_read_all();  // earlier stores no longer read this stage
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint32_t bg = (uint32_t)(len * sizeof(T)), bf = (uint32_t)(len * 4);
+    mbar_expect_tx(&full[st], bg + 2 * bf);
+    tma_load_1d(base(st), g + e0, bg, &full[st]);
+    tma_load_1d(base(st) + kG, mom + e0, bf, &full[st]);
+    tma_load_1d(base(st) + kG + kF, ref + e0, bf, &full[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t c = c_begin; c < min(c_end, c_begin + kUpdTmaStages - 1); ++c) issue_load(c);
+  for (int64_t c = c_begin; c < c_end; ++c) {
+    const int st = (int)((c - c_begin) % kUpdTmaStages);
+    const uint32_t parity = (uint32_t)(((c - c_begin) / kUpdTmaStages) & 1);
+    if (threadIdx.x == 0 && c + kUpdTmaStages - 1 < c_end) issue_load(c + kUpdTmaStages - 1);
+    mbar_wait(&full[st], parity);
+    int64_t e0, len;
+    chunk_range(c, &e0, &len);
+    const T* sg = reinterpret_cast<const T*>(base(st));
+    float* sv = reinterpret_cast<float*>(base(st) + kG);
+    float* sp = reinterpret_cast<float*>(base(st) + kG + kF);
+    T* so = reinterpret_cast<T*>(base(st) + kG + 2 * kF);
+    for (int64_t i = threadIdx.x * 4; i < len; i += (int64_t)blockDim.x * 4) {
+      const float4 g4 = load4(sg + i);
+      float4 m4 = *reinterpret_cast<float4*>(sv + i);
+      float4 p4 = *reinterpret_cast<float4*>(sp + i);
+      m4.x = fmaf(momentum, m4.x, g4.x * scale);
+      m4.y = fmaf(momentum, m4.y, g4.y * scale);
+      m4.z = fmaf(momentum, m4.z, g4.z * scale);
+      m4.w = fmaf(momentum, m4.w, g4.w * scale);
+      p4.x = fmaf(-lr, m4.x, p4.x);
+      p4.y = fmaf(-lr, m4.y, p4.y);
+      p4.z = fmaf(-lr, m4.z, p4.z);
+      p4.w = fmaf(-lr, m4.w, p4.w);
+      *reinterpret_cast<float4*>(sv + i) = m4;
+      *reinterpret_cast<float4*>(sp + i) = p4;
+      if (kMaster) store4(so + i, p4);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t bf = (uint32_t)(len * 4), bo = (uint32_t)(len * sizeof(T));
+      tma_store_1d(mom + e0, sv, bf);
+      if (kMaster) {
+        tma_store_1d(ref + e0, sp, bf);
+#pragma unroll
+        for (int k = 0; k < W; ++k) tma_store_1d(dst[k] + e0, so, bo);
+      } else {
+#pragma unroll
+        for (int k = 0; k < W; ++k) tma_store_1d(dst[k] + e0, sp, bo);
+      }
+      tma_store_commit();
+    }
+  }
+  if (threadIdx.x == 0) {
+    tma_store_wait_all();  // every bulk store of this CTA performed (incl. peers)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  // exit: every rank's stores into every parameter buffer have landed
+  peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 2u);
+}
+
+bool launch_update_allgather_tma(const PeerPtrs& P, int rank, int world, int dtype,
+                                 int64_t slot_base, int32_t count, const int64_t* offsets,
+                                 const int64_t* numels, float lr, float momentum,
+                                 float grad_scale, float* mom, int max_blocks,
+                                 cudaStream_t stream) {
+  static int enabled = [] {
+    const char* e = getenv("DEFT_UPDATE_IMPL");
+    return e && e[0] == 'l' ? 0 : 1;   // default: TMA
+  }();
+  if (!enabled || world < 2) return false;
+  const int align = dtype == 0 ? 4 : 8;
+  for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
+    ChunkTable t{};
+    t.count = count - s0 < kMaxSeg ? count - s0 : kMaxSeg;
+    t.first[0] = 0;
+    int64_t total_elems = 0;
+    for (int k = 0; k < t.count; ++k) {
+      const ShardRange sh = shard_of(offsets[s0 + k], numels[s0 + k], rank, world, align);
+      int64_t a = (sh.lo + 7) / 8 * 8;
+      if (a > sh.hi) a = sh.hi;
+      int64_t b = sh.hi / 8 * 8;
+      if (b < a) b = a;
+      t.head_lo[k] = sh.lo; t.head_hi[k] = a;
+      t.tail_lo[k] = b; t.tail_hi[k] = sh.hi;
+      t.off[k] = a;
+      t.len[k] = b - a;
+      t.first[k + 1] = t.first[k] + (t.len[k] + kUpdChunk - 1) / kUpdChunk;
+      total_elems += numels[s0 + k];
+    }
+    int grid = comm_grid_for((total_elems + world - 1) / world);
+    if (max_blocks > 0 && grid > max_blocks) grid = max_blocks;
+    const size_t esz = dtype == 0 ? 4 : 2;
+    const size_t smem = (size_t)kUpdTmaStages *
+                        (kUpdChunk * esz + 2 * kUpdChunk * 4 + (dtype == 0 ? 0 : kUpdChunk * esz));
+#define DEFT_UPT_CASE(WW)                                                                      \
+  case WW:                                                                                     \
+    if (dtype == 0) {                                                                          \
+      cudaFuncSetAttribute(update_allgather_tma_kernel<float, WW>,                             \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+      update_allgather_tma_kernel<float, WW><<<grid, kUpdTmaThreads, smem, stream>>>(          \
+          P, rank, slot_base, t, lr, momentum, grad_scale, mom);                               \
+    } else {                                                                                   \
+      cudaFuncSetAttribute(update_allgather_tma_kernel<__nv_bfloat16, WW>,                     \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+      update_allgather_tma_kernel<__nv_bfloat16, WW><<<grid, kUpdTmaThreads, smem, stream>>>(  \
+          P, rank, slot_base, t, lr, momentum, grad_scale, mom);                               \
+    }                                                                                          \
+    break;
+    switch (world) {
+      DEFT_UPT_CASE(2) DEFT_UPT_CASE(3) DEFT_UPT_CASE(4) DEFT_UPT_CASE(5)
+      DEFT_UPT_CASE(6) DEFT_UPT_CASE(7) DEFT_UPT_CASE(8)
+      default: break;
+    }
+#undef DEFT_UPT_CASE
+    count_launch();
+  }
   return true;
 }
 
