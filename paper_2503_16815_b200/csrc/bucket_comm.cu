@@ -303,13 +303,33 @@ cudaError_t launch_barrier(const PeerPtrs& P, int rank, int world, int set,
   return cudaGetLastError();
 }
 
-// CE channel local reduce: own shard += staged peer shards.
+// CE channel local reduce: own shard += staged peer shards (128-bit accesses;
+// the staged copies and the own shard share their alignment).
 template <typename T>
 __global__ void __launch_bounds__(kLocalThreads) ce_reduce_kernel(
     T* own, const T* staging, int world, int rank, int64_t len, int64_t stride_elems) {
   using V = Vec<T>;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  using Raw = typename V::Raw;
+  const int64_t nv = ((reinterpret_cast<uintptr_t>(own) % 16) == 0 &&
+                      (reinterpret_cast<uintptr_t>(staging) % 16) == 0 &&
+                      (stride_elems % V::N) == 0) ? len / V::N : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
+    float acc[V::N], tmp[V::N];
+    V::to_f32(reinterpret_cast<const Raw*>(own)[v], acc);
+    int slot = 0;
+    for (int k = 0; k < world; ++k) {
+      if (k == rank) continue;
+      V::to_f32(__ldg(reinterpret_cast<const Raw*>(staging + (int64_t)slot * stride_elems) + v),
+                tmp);
+#pragma unroll
+      for (int c = 0; c < V::N; ++c) acc[c] += tmp[c];
+      ++slot;
+    }
+    reinterpret_cast<Raw*>(own)[v] = V::from_f32(acc);
+  }
+  for (int64_t e = nv * V::N + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len;
+       e += stride) {  // scalar remainder
     float acc = V::scalar(own + e);
     int slot = 0;
     for (int k = 0; k < world; ++k) {

@@ -398,7 +398,7 @@ extern "C" deft_status_t deft_bucket_reduce_scatter(deft_comm* c, int32_t channe
   const int esz = c->dtype == DEFT_DTYPE_F32 ? 4 : 2;
   const ShardRange sh = shard_of(offset, numel, c->rank, c->world, c->dtype == 0 ? 4 : 8);
   const int64_t len = sh.hi - sh.lo;
-  const int64_t per = (numel + c->world - 1) / c->world + 16;
+  const int64_t per = ((numel + c->world - 1) / c->world + 16 + 7) / 8 * 8;  // 16-B strides
   const size_t need = (size_t)(c->world - 1) * per * esz;
   if (need > c->staging_bytes) {
     if (c->staging) {
