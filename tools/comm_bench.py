@@ -48,6 +48,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes-mb", default="1,4,16,64,256")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--update-blocks", type=int, default=0,
+                    help="CTA budget of the update kernels (0 = default)")
     ap.add_argument("--check", action="store_true",
                     help="verify every reduce-scatter result before timing")
     args = ap.parse_args()
@@ -60,6 +62,7 @@ def main():
     max_elems = max(sizes) * 2**20 // 4
     comm = BucketComm(rank, W, 1, max_elems, torch.float32, dev)
     comm.grads.normal_()
+    comm.set_update_blocks(args.update_blocks)
     mom = torch.zeros(max_elems, device=dev)
     s = torch.cuda.Stream(dev)
     rows = []
@@ -88,12 +91,14 @@ def main():
                                      args.reps, 3, s, dev)
             res["rs_ce_ms"] = timeit(lambda: comm.reduce_scatter(_native.CHANNEL_CE, 0, 0, n, s),
                                      args.reps, 3, s, dev)
-            res["upd_ag_ms"] = timeit(lambda: comm.update(0, 0, n, 1e-9, 0.9, 1e-3, mom, s),
-                                      args.reps, 3, s, dev)
+            # the multi-bucket entry point: the TMA-pipelined update kernel
+            res["upd_ag_ms"] = timeit(
+                lambda: comm.update_multi(0, [(0, n)], 1e-3, 1e-9, 0.9, mom, s),
+                args.reps, 3, s, dev)
 
             def deft():
                 comm.reduce_scatter(_native.CHANNEL_SM, 0, 0, n, s)
-                comm.update(0, 0, n, 1e-9, 0.9, 1e-3, mom, s)
+                comm.update_multi(0, [(0, n)], 1e-3, 1e-9, 0.9, mom, s)
             res["deft_ms"] = timeit(deft, args.reps, 3, s, dev)
             x = torch.randn(n, device=dev)
             p = torch.randn(n, device=dev)
