@@ -48,6 +48,9 @@ def parse():
                     choices=["auto", "bucket", "end", "start"])
     ap.add_argument("--update-blocks", type=int, default=0,
                     help="CTA budget of the update kernels (0 = default)")
+    ap.add_argument("--scheme", default="deft", choices=["deft", "wfbp", "priority"],
+                    help="schedule run on the executor: DeFT, or one of the reference's "
+                         "synchronous baselines (scheduler.py:386-418) on the same kernels")
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs")
     ap.add_argument("--bucket-mb", type=float, default=None,
                     help="partition size in MB of fp32 (default: the reference's 6.5M params)")
@@ -516,7 +519,7 @@ def main():
     cfg = D.DeftConfig(lr=0.1, momentum=0.9, walk=walk,
                        cuda_graphs=False if args.eager else "auto",
                        update_placement=args.update_placement,
-                       update_blocks=args.update_blocks,
+                       update_blocks=args.update_blocks, scheme=args.scheme,
                        autocast_dtype=None if args.model == "gpt2" else torch.bfloat16,
                        partition=D.PartitionConfig(partition_size=psize, mu=1.0))
     ddp = D.DeftDataParallel(model, cfg)
@@ -668,14 +671,17 @@ def main():
             # arithmetic of the DeFT path itself: gradient reduce + SGD/momentum update
             "dtype": "bf16" if ddp.cfg.grad_dtype == torch.bfloat16 else "f32",
             "data": "synthetic (random-init weights, randn images / random tokens)",
-            "config": {"workload": f"{args.model} DeFT delayed-update DP, batch "
+            "config": {"workload": f"{args.model} " + (
+                           "DeFT delayed-update DP" if args.scheme == "deft" else
+                           f"{args.scheme} synchronous DP (reference baseline schedule)") +
+                       ", batch "
                                    f"{args.batch}/GPU" + (", 224x224" if args.model != "gpt2"
                                                            else ", seq 1024"),
                        "model": args.model, "global_batch": args.batch * world,
                        "parallelism": f"dp{world}", "l2": "working set (activations) >> L2 126 MB",
                        "grad_dtype": str(ddp.cfg.grad_dtype).replace("torch.", ""),
                        "compute": "bf16 autocast" if args.model != "gpt2" else "bf16 weights",
-                       "update_placement": ddp.placement,
+                       "scheme": args.scheme, "update_placement": ddp.placement,
                        "buckets": part.n_buckets, "links": [l.name for l in ddp.cluster.links],
                        "capacity_multiplier": ddp.capacity_multiplier,
                        "partition_size": psize, "comm_scale": args.comm_scale,

@@ -10,7 +10,9 @@ arithmetic, which SURVEY.md §8c fixes (and DESIGN.md restates):
     (the k*B*W mean, preserver.py:93-94, PAPER.md:378-388);
   * the step is torch.optim.SGD momentum: v <- m*v + g ; theta <- theta - lr*v
     (dampening 0, no nesterov, no weight decay);
-  * events of decision (t, backward) are visible from iteration t+2.
+  * events of decision (t, backward) are visible from iteration t+2 (``lag=2``);
+    the synchronous baseline schedules (wfbp / priority, ``delayed_updates=False``,
+    scheduler.py:386-418) make them visible from t+1 (``lag=1``).
 
 ``reduce`` selects how the per-rank gradients are summed: "local" (all ranks'
 gradients are known to the caller) or "gloo" (this process is one rank of an
@@ -34,7 +36,7 @@ def events_by_iteration(decisions) -> dict[int, list[tuple[tuple[int, ...], int]
 
 def run(theta0: torch.Tensor, grad_of: Callable[[torch.Tensor, int, int], torch.Tensor],
         decisions, world: int, lr: float, momentum: float, iterations: int,
-        reduce: str = "local", rank: int = 0) -> torch.Tensor:
+        reduce: str = "local", rank: int = 0, lag: int = 2) -> torch.Tensor:
     """Return theta^(iterations): the parameters the next forward would use.
 
     grad_of(theta, rank, t) -> this rank's flat fp32 gradient at iteration t,
@@ -45,7 +47,7 @@ def run(theta0: torch.Tensor, grad_of: Callable[[torch.Tensor, int, int], torch.
     events = events_by_iteration(decisions)
     summed: dict[int, torch.Tensor] = {}
     for s in range(iterations + 1):
-        for origins, k in events.get(s - 2, ()):
+        for origins, k in events.get(s - lag, ()):
             g = torch.zeros_like(theta)
             for o in origins:
                 g += summed.pop(o)

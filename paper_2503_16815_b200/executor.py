@@ -41,11 +41,14 @@ import torch
 from . import _native
 from .comm import BucketComm
 from .errors import DeftError, InternalInvariantError
-from .partition import PartitionConfig, element_ranges, partition_buckets
+from .partition import PartitionConfig, element_ranges, partition_buckets, partition_by_size
 from .preserver import WalkParams, feedback_loop
 from .profiles import BucketProfile, ClusterSpec, LinkSpec, ModelProfile
 from .planner import ExecutionPlanner, IterPlan
-from .scheduler import DeftScheduler, ScheduleDecision
+from .scheduler import (DeftScheduler, OrderScheduler, ScheduleDecision, priority_order,
+                        wfbp_order)
+
+SCHEMES = ("deft", "wfbp", "priority")
 
 
 @dataclass
@@ -72,11 +75,16 @@ class DeftConfig:
     # "start" = at the start of the iteration it becomes visible in, input-side
     #           bucket first, each bucket's forward waiting only for its own update
     update_placement: str = "auto"
-    # CTAs of every update kernel (0 = the comm default; 16 with "start").  With
+    # CTAs of every update kernel (0 = the comm default; 32 with "start").  With
     # "start" placement a small budget lets the update overlap the forward instead
     # of displacing it.
     update_blocks: int = 0
     start_groups: int = 8                   # update launches per event with "start"
+    # "deft" (delayed updates) or one of the reference's synchronous baselines on
+    # the same kernels (scheduler.py:386-418): "wfbp" (every bucket at its own
+    # backward end, measured buckets) / "priority" (partition_by_size blocks,
+    # input layer first).  Synchronous: updates of iteration t visible from t+1.
+    scheme: str = "deft"
     graph_warmup: int = 1                   # eager runs of a shape before it is captured
 
 
@@ -106,6 +114,9 @@ class DeftDataParallel:
             self.placement = "end" if self.world == 1 else "start"
         if self.placement not in ("end", "start", "bucket"):
             raise DeftError(f"unknown update placement {self.placement!r}")
+        if self.cfg.scheme not in SCHEMES:
+            raise DeftError(f"unknown scheme {self.cfg.scheme!r}")
+        self.sync = self.cfg.scheme != "deft"
         if self.device.type != "cuda":
             raise DeftError("DeftDataParallel runs on CUDA devices only (no CPU fallback)")
         # DDP order: output-side parameter first (bucket 1 finishes backward first)
@@ -323,11 +334,16 @@ class DeftDataParallel:
                                     for l in cluster.links]
         mult = self.cfg.capacity_multiplier
         self.verdict = None
-        if self.cfg.walk is not None:
+        if self.cfg.walk is not None and not self.sync:
             _, self.verdict = feedback_loop(profile, cluster, self.cfg.partition, self.cfg.walk,
                                             iterations=feedback_iterations)
             mult = self.verdict.capacity_multiplier
-        part = partition_buckets(profile, self.cfg.partition)
+        if self.cfg.scheme == "wfbp":
+            part = profile
+        elif self.cfg.scheme == "priority":
+            part = partition_by_size(profile, self.cfg.partition.partition_size)
+        else:
+            part = partition_buckets(profile, self.cfg.partition)
         if part.total_param_count != self.total:
             raise DeftError(f"profile covers {part.total_param_count} parameters, "
                             f"model has {self.total}")
@@ -345,16 +361,23 @@ class DeftDataParallel:
         self._gather_slot = None
         from .gpu_scheduler import KernelScheduler
         from .scheduler import use_kernel_engine
-        if (use_kernel_engine(self.cfg.schedule_engine)
+        if self.sync:
+            order = wfbp_order(part) if self.cfg.scheme == "wfbp" else priority_order(part)
+            self.scheduler = OrderScheduler(part, cluster.fast_link.name, order,
+                                            link=cluster.links.index(cluster.fast_link))
+        elif (use_kernel_engine(self.cfg.schedule_engine)
                 and KernelScheduler.supported(part, cluster, mult)):
             self.scheduler = KernelScheduler(part, cluster, mult)   # K5, in chunks
         else:
             self.scheduler = DeftScheduler(part, cluster, mult)
         self.capacity_multiplier = mult
-        blocks = self.cfg.update_blocks or (16 if self.placement == "start" else 0)
+        blocks = self.cfg.update_blocks or (32 if self.placement == "start" else 0)
         self.comm.set_update_blocks(blocks)
+        # delayed (DeFT): visible from t+2; synchronous baselines: from t+1
+        lag = (1 if self.placement == "start" else 0) if self.sync else \
+            (2 if self.placement == "start" else 1)
         self.planner = ExecutionPlanner(self.scheduler, self.cfg.n_slots, self.cfg.lookahead,
-                                        lag=2 if self.placement == "start" else 1)
+                                        lag=lag)
         self.link_streams = [torch.cuda.Stream(self.device) for _ in cluster.links]
         # runtime state
         self._slot_free = [None] * self.cfg.n_slots   # event: slot reusable (async mode)
@@ -426,7 +449,9 @@ class DeftDataParallel:
         self._timed("reduce_scatter", s,
                     lambda: self.comm.reduce_scatter(self.channel_of_link[link], slot, b.lo,
                                                      b.hi - b.lo, s), nbytes)
-        if not self._sequential:
+        if not self._sequential or self.planner.lag == 0:
+            # an update waits for it: always when streams run ahead (eager, async),
+            # and within the iteration for synchronous schedules (lag 0)
             ev = torch.cuda.Event()
             ev.record(s)
             self._rs_done[(slot, bidx)] = ev
@@ -532,6 +557,11 @@ class DeftDataParallel:
         else:
             nbytes = self.total * esz * (self.world - 1) // self.world  # crossing NVLink
         for slot, k in self._due_now:
+            if self.world > 1:   # the group's reduce-scatters still in flight
+                for b in range(len(self.buckets)):
+                    rs = self._rs_done.pop((slot, b), None)
+                    if rs is not None:
+                        comp.wait_event(rs)
             self._timed("update", comp, lambda: self.comm.update_multi(
                 slot, ranges, 1.0 / (self.world * k), self.cfg.lr, self.cfg.momentum, self.mom,
                 comp), nbytes)

@@ -31,15 +31,17 @@ class IterPlan:
 
 
 class ExecutionPlanner:
-    """``lag`` = how many iterations after its decision an update event is applied:
-    1 -> during the next backward ("end"/"bucket" placement), 2 -> at the start of
-    the iteration it becomes visible in ("start" placement).  Either way the update
-    of decision (t, backward) is visible from iteration t+2."""
+    """``lag`` = how many iterations after its decision an update event is applied.
+    Delayed schedules (DeFT, visible from t+2): 1 -> during the next backward
+    ("end"/"bucket" placement), 2 -> at the start of the iteration it becomes
+    visible in ("start" placement).  Synchronous schedules (the wfbp / priority
+    baselines, ``delayed_updates=False``, visible from t+1): 0 -> in the same
+    backward, 1 -> at the start of the next iteration."""
 
     def __init__(self, scheduler: DeftScheduler, n_slots: int, lookahead: int = 32,
                  lag: int = 1):
-        if lag not in (1, 2):
-            raise InternalInvariantError("update lag must be 1 or 2")
+        if lag not in (0, 1, 2):
+            raise InternalInvariantError("update lag must be 0, 1 or 2")
         self.scheduler = scheduler
         self.n_slots = n_slots
         self.lookahead = lookahead
@@ -77,7 +79,7 @@ class ExecutionPlanner:
         """("start" placement) updates that are due at the start of the NEXT
         iteration, handed out early so a caller can make theta^(t) current
         without running iteration t.  Returns (due, freed)."""
-        if self.lag != 2 or len(self._event_queue) < self.lag:
+        if self.lag == 0 or len(self._event_queue) < self.lag:
             return (), ()
         due_groups = self._event_queue.pop(0)
         due = tuple((self._slot_of[u], k) for u, k in due_groups)
@@ -116,14 +118,14 @@ class ExecutionPlanner:
                 else:
                     bwd.append((tr.link, slot, tr.bucket_id - 1))
         # groups reported by decision (t-lag, backward) are updated in this iteration
-        due_groups = self._event_queue.pop(0) if len(self._event_queue) >= self.lag else []
+        self._event_queue.append([(u, k) for u, k, _ in dB.exec.updates])
+        due_groups = self._event_queue.pop(0) if len(self._event_queue) > self.lag else []
         due = tuple((self._slot_of[u], k) for u, k in due_groups)
         freed = []
         for u, _ in due_groups:
             s = self._slot_of.pop(u)
             self._busy[s] = False
             freed.append(s)
-        self._event_queue.append([(u, k) for u, k, _ in dB.exec.updates])
         fresh_t = tuple(sorted((b, tuple(v)) for b, v in fresh.items()))
         key = (fwd, slot, new, tuple(bwd), fresh_t, due)
         return IterPlan(t, slot, new, fwd, tuple(bwd), fresh_t, due, tuple(freed), key)

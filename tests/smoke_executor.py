@@ -73,13 +73,13 @@ def equal_dual():
 
 def run_executor(world, rank, iterations, n_buckets=48, total=48_000, lr=0.05, momentum=0.9,
                  dtype=torch.float32, comm_us=900, group=None, cuda_graphs=True,
-                 grad_fn=flat_grad, placement="end"):
+                 grad_fn=flat_grad, placement="end", scheme="deft", partition_size=10**9):
     """Run the executor on the probe; return (theta^(T) flat fp32 CPU -- the fp32
     master for bf16 models --, theta0, decisions as dicts[, bf16 params])."""
     model = Probe(probe_sizes(total)).cuda().to(dtype)
     cfg = D.DeftConfig(lr=lr, momentum=momentum, autocast_dtype=None,
-                       partition=D.PartitionConfig(partition_size=10**9),
-                       cuda_graphs=cuda_graphs, update_placement=placement)
+                       partition=D.PartitionConfig(partition_size=partition_size),
+                       cuda_graphs=cuda_graphs, update_placement=placement, scheme=scheme)
     ddp = D.DeftDataParallel(model, cfg, process_group=group)
     prof = uniform_profile(n_buckets, total // n_buckets, comm_us=comm_us)
     ddp.plan(prof, equal_dual())
@@ -106,9 +106,10 @@ def run_executor(world, rank, iterations, n_buckets=48, total=48_000, lr=0.05, m
 
 
 def oracle_theta(theta0, decisions, world, iterations, total=48_000, lr=0.05, momentum=0.9,
-                 grad_fn=flat_grad):
+                 grad_fn=flat_grad, lag=2):
+    """lag 2: DeFT (visible from t+2); lag 1: the synchronous wfbp/priority schemes."""
     return delayed_sgd.run(theta0, lambda th, r, t: grad_fn(total, r, t), decisions, world,
-                           lr, momentum, iterations)
+                           lr, momentum, iterations, lag=lag)
 
 
 def rel_err(a, b):

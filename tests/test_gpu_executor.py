@@ -27,6 +27,24 @@ def test_single_gpu_matches_oracle(iterations, comm_us, graphs, placement):
     assert S.rel_err(theta, want) <= S.TOL
 
 
+@pytest.mark.parametrize("scheme", ["wfbp", "priority"])
+@pytest.mark.parametrize("placement", ["end", "bucket", "start"])
+@pytest.mark.parametrize("graphs", [True, False])
+def test_single_gpu_synchronous_baselines(scheme, placement, graphs):
+    """The reference's synchronous schedules (scheduler.py:386-418) on the same
+    executor and kernels: updates of iteration t visible from t+1 (oracle lag 1).
+    priority: partition_by_size blocks (1000-element buckets cut into 334/333/333)."""
+    iters = 12
+    theta, theta0, decisions = S.run_executor(
+        1, 0, iters, cuda_graphs=graphs, placement=placement, scheme=scheme,
+        partition_size=400 if scheme == "priority" else 10**9)
+    assert all(u["merge_count"] == 1 for d in decisions for u in d["update_events"])
+    want = S.oracle_theta(theta0, decisions, 1, iters, lag=1)
+    assert S.rel_err(theta, want) <= S.TOL
+    # and it is NOT the delayed trajectory
+    assert S.rel_err(theta, S.oracle_theta(theta0, decisions, 1, iters, lag=2)) > 1e-4
+
+
 @pytest.mark.parametrize("placement", ["end", "start"])
 @pytest.mark.parametrize("graphs", [True, False])
 def test_bf16_params_single_gpu(graphs, placement):
@@ -50,7 +68,8 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, iterations, comm_us, graphs, q, bf16=False, placement="end"):
+def _worker(rank, world, port, iterations, comm_us, graphs, q, bf16=False, placement="end",
+            scheme="deft"):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
@@ -63,8 +82,10 @@ def _worker(rank, world, port, iterations, comm_us, graphs, q, bf16=False, place
                 dtype=torch.bfloat16, grad_fn=S.flat_grad_dyadic, placement=placement)
             q.put((rank, theta, theta0, decisions, params))
         else:
-            theta, theta0, decisions = S.run_executor(world, rank, iterations, comm_us=comm_us,
-                                                      cuda_graphs=graphs, placement=placement)
+            theta, theta0, decisions = S.run_executor(
+                world, rank, iterations, comm_us=comm_us, cuda_graphs=graphs,
+                placement=placement, scheme=scheme,
+                partition_size=400 if scheme == "priority" else 10**9)
             q.put((rank, theta, theta0, decisions))
     finally:
         dist.destroy_process_group()
@@ -100,6 +121,39 @@ def test_multi_gpu_matches_oracle(iterations, comm_us, graphs, placement):
         assert res[r][2] == decisions          # every rank planned the same stream
         assert S.rel_err(res[r][0], want) <= S.TOL, r
         assert torch.equal(res[r][0], res[0][0])  # replicas bit-identical
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("scheme,graphs,placement", [
+    ("wfbp", True, "end"), ("wfbp", False, "bucket"), ("priority", True, "start"),
+    ("priority", False, "end")])
+def test_multi_gpu_synchronous_baselines(scheme, graphs, placement):
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    iterations = 10
+    ctx = torch.multiprocessing.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, iterations, 900, graphs, q,
+                                             False, placement, scheme))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, theta, theta0, decisions = q.get(timeout=300)
+        res[r] = (theta, theta0, decisions)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    theta0, decisions = res[0][1], res[0][2]
+    want = S.oracle_theta(theta0, decisions, world, iterations, lag=1)
+    for r in range(world):
+        assert res[r][2] == decisions
+        assert S.rel_err(res[r][0], want) <= S.TOL, r
+        assert torch.equal(res[r][0], res[0][0])
 
 
 def shard_range(offset, numel, r, world, align):

@@ -29,13 +29,17 @@ def check_invariants(planner, n_buckets, iters):
     the decision reporting it, once all its buckets were sent; <= n_slots live."""
     live = {}        # slot -> set of bucket indices still to transfer
     reported = {}    # slot -> (iteration of the reporting decision, merge_count)
-    for t in range(iters):
-        p = planner.plan(t)
+    def apply_due(t, p):
         for slot, k in p.due:
             it, kk = reported.pop(slot)
             assert (it, kk) == (t - planner.lag, k), (t, slot)
             del live[slot]
         assert sorted(p.freed) == sorted(s for s, _ in p.due)
+
+    for t in range(iters):
+        p = planner.plan(t)
+        if planner.lag > 0:
+            apply_due(t, p)
         for link, slot, b in p.fwd + p.bwd:
             assert slot in live and b in live[slot], (t, slot, b)
             live[slot].discard(b)
@@ -54,6 +58,8 @@ def check_invariants(planner, n_buckets, iters):
         for (uid, k, _), s_ in zip(d_b.exec.updates, done):
             reported[s_] = (t, k)
         assert len(live) <= planner.n_slots
+        if planner.lag == 0:      # synchronous: this iteration's own group
+            apply_due(t, p)
 
 
 @pytest.fixture(autouse=True)
@@ -72,6 +78,32 @@ def test_planner_invariants_on_golden_streams(golden_index, golden_inputs, lag):
         check_invariants(planner, part.n_buckets, min(iters, 120))
         checked += 1
     assert checked >= 45
+
+
+@pytest.mark.parametrize("scheme", ["wfbp", "priority"])
+@pytest.mark.parametrize("lag", [0, 1])
+def test_planner_synchronous_baselines(golden_inputs, scheme, lag):
+    """The reference's synchronous baselines (scheduler.py:386-418) through the
+    same planner: one store per iteration, every bucket fresh on the fast link,
+    the group updated `lag` iterations later in one shape (one CUDA graph)."""
+    from paper_2503_16815_b200.scheduler import OrderScheduler, priority_order, wfbp_order
+    for name in ("resnet101", "vgg19", "gpt2"):
+        prof = D.profile_from_dict(golden_inputs["profiles"][name])
+        cluster = D.cluster_from_dict(golden_inputs["clusters"]["dual"])
+        if scheme == "priority":
+            prof = D.partition_by_size(prof, 6_500_000)
+        order = wfbp_order(prof) if scheme == "wfbp" else priority_order(prof)
+        sched = OrderScheduler(prof, cluster.fast_link.name, order)
+        # the decision stream is the reference's (golden-checked via build_schedule)
+        ref = (D.baseline_wfbp(prof, cluster, 6) if scheme == "wfbp" else
+               D.baseline_priority(prof, cluster, D.PartitionConfig(6_500_000), 6))
+        assert sched.run(6) == list(ref.decisions)
+        planner = ExecutionPlanner(sched, 3, lag=lag)
+        check_invariants(planner, prof.n_buckets, 30)
+        keys = [planner.plan(t).key for t in range(30, 40)]
+        assert len(set(keys)) <= 2, (name, scheme)
+        p = planner.plan(40)
+        assert p.zero and len(p.fresh) == prof.n_buckets and not p.fwd and not p.bwd
 
 
 def test_steady_state_shapes_are_few(golden_inputs):
