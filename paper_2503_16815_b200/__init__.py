@@ -18,6 +18,7 @@ from .knapsack import (MAX_EXACT_CAPACITY, Item, KnapsackAssignment, brute_force
                        greedy_multi_knapsack, naive_knapsack, recursive_knapsack)
 from .partition import (DEFAULT_PARTITION_SIZE, PartitionConfig, comm_capacity_bound_us,
                         fuse_buckets, partition_buckets, partition_by_size)
+from .experiment import RunReport, compare, emit_reports, load_experiment_config
 from .preserver import (BatchSequence, ConvergenceVerdict, WalkParams, baseline_expected_state,
                         check_sequence, expected_next_state, extract_batch_sequence,
                         feedback_loop, sequence_expected_state)

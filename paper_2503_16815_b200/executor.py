@@ -141,6 +141,7 @@ class DeftDataParallel:
         self.schedule_profile: ModelProfile | None = None
         self.cluster: ClusterSpec | None = None
         self.iteration = 0
+        self.updates_applied = 0                # update events issued so far
         self._events_t: list[tuple[str, torch.cuda.Event, torch.cuda.Event, int]] = []
 
     # ------------------------------------------------------------------ setup
@@ -330,8 +331,12 @@ class DeftDataParallel:
             raise DeftError("measure_profile() or an explicit profile/cluster is required")
         if cluster is not self.cluster:
             self.cluster = cluster
-            self.channel_of_link = [_native.CHANNEL_SM if l.is_fast else _native.CHANNEL_CE
-                                    for l in cluster.links]
+            # measured links carry their channel in the name (_make_links); any
+            # other cluster: the fast link is the SM channel, the rest copy engines
+            self.channel_of_link = [
+                _native.CHANNEL_CE if l.name == "nvlink_ce" else
+                _native.CHANNEL_SM if l.name == "nvlink_sm" or l.is_fast else
+                _native.CHANNEL_CE for l in cluster.links]
         mult = self.cfg.capacity_multiplier
         self.verdict = None
         if self.cfg.walk is not None and not self.sync:
@@ -706,6 +711,7 @@ class DeftDataParallel:
             self._param_index = {id(p): i for i, p in enumerate(self.params)}
         it = self.planner.plan(self.iteration)
         self.iteration += 1
+        self.updates_applied += len(it.due)
         caller = torch.cuda.current_stream(self.device)
         self.compute_stream.wait_stream(caller)
         with torch.cuda.stream(self.compute_stream):
@@ -805,6 +811,7 @@ class DeftDataParallel:
         iterations are still in flight."""
         if self.placement == "start" and hasattr(self, "planner"):
             due, freed = self.planner.take_pending()
+            self.updates_applied += len(due)
             if due:
                 caller = torch.cuda.current_stream(self.device)
                 self.compute_stream.wait_stream(caller)

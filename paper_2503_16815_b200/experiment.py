@@ -1,0 +1,499 @@
+"""Experiments on the B200 with the reference's report schema.
+
+The reference plans and SIMULATES an experiment grid -- schemes x sweep points --
+and writes ``summary.json`` / ``comparison.csv`` / ``plotdata/*.csv``
+(cli.py:52-391).  This module reads the same experiment JSON, RUNS every
+(scheme, point) on the GPUs through ``DeftDataParallel`` and writes the same
+files from measured CUDA-event timings, so simulator-vs-hardware comparisons
+line up column for column.
+
+What the fields mean on hardware (``RunReport.from_measurement``):
+  * ``total_time_us``          CUDA-event time of the ``iterations`` timed steps
+                               (max over ranks);
+  * ``mean_iteration_time_us`` total / iterations;
+  * ``bubble_time_us``         time the steps exceed the compute-only step (one
+                               GPU's forward + backward [+ local optimizer step],
+                               no communication), i.e. exposed
+                               communication -- the simulator's compute idle time
+                               (simulator.py:250-256);
+  * ``updates_performed``      update events applied inside the timed steps;
+  * ``throughput_samples_per_s`` per-GPU samples/s (profile batch size, as
+                               simulator.py:258).
+Sweep axes: ``partition_size`` re-partitions the real buckets; ``bandwidth_scale``
+scales the PLANNED communication times (the schedule DeFT computes), the
+links themselves run at NVLink speed; ``gpu_count`` points other than the
+launched world size are skipped.  ``nonsequential`` is the simulator-scored
+search baseline (scheduler.py:421-472) and is not run.
+"""
+from __future__ import annotations
+
+import csv
+import hashlib
+import json
+from dataclasses import dataclass, field, replace
+from pathlib import Path
+from typing import Callable
+
+from .errors import ComparisonError, SchemaError
+from .partition import PartitionConfig
+from .preserver import WalkParams, check_sequence, extract_batch_sequence
+from .profiles import ClusterSpec, ModelProfile
+from .scheduler import SCHEMES, Schedule
+
+HW_SCHEMES = ("wfbp", "priority", "deft", "deft_single_link")
+
+
+# ----------------------------------------------------------------- config (cli.py:52-175)
+
+@dataclass(frozen=True)
+class SweepPoint:
+    """One point of the experiment grid; the base point changes nothing (cli.py:52-67)."""
+
+    bandwidth_scale: float = 1.0
+    partition_size: int | None = None
+    gpu_count: int | None = None
+
+    def label(self) -> str:
+        parts = []
+        if self.bandwidth_scale != 1.0:
+            parts.append(f"bw{self.bandwidth_scale:g}")
+        if self.partition_size is not None:
+            parts.append(f"ps{self.partition_size}")
+        if self.gpu_count is not None:
+            parts.append(f"gpu{self.gpu_count}")
+        return "_".join(parts) or "base"
+
+
+@dataclass(frozen=True)
+class ExperimentConfig:
+    """cli.py:70-85 (the ``sim`` block is simulator-only and ignored here)."""
+
+    profile_path: str
+    cluster_path: str | None
+    cluster_inline: dict | None
+    schemes: tuple[str, ...]
+    iterations: int
+    partition: PartitionConfig
+    walk: WalkParams | None
+    bandwidth_scales: tuple[float, ...] = ()
+    partition_sizes: tuple[int, ...] = ()
+    gpu_counts: tuple[int, ...] = ()
+
+
+def experiment_config_from_dict(data: dict, base_dir: Path) -> ExperimentConfig:
+    """Same fields, defaults and SchemaError messages as cli.py:100-143."""
+    if not isinstance(data, dict):
+        raise SchemaError("experiment config must be a JSON object")
+    for key in ("profile", "schemes", "iterations"):
+        if key not in data:
+            raise SchemaError(f"experiment config: missing field {key!r}")
+    unknown = [s for s in data["schemes"] if s not in SCHEMES]
+    if unknown:
+        raise SchemaError(f"unknown schemes: {unknown}")
+    part = data.get("partition", {})
+    partition = PartitionConfig(
+        partition_size=int(part.get("partition_size", 6_500_000)),
+        mu=float(part.get("mu", 1.0)),
+        enable_fusion=bool(part.get("enable_fusion", False)),
+        comm_startup_us=int(part.get("comm_startup_us", 0)),
+    )
+    walk = WalkParams.from_dict(data["walk"]) if "walk" in data else None
+    sweeps = data.get("sweeps", {})
+    for axis in ("bandwidth_scale", "partition_size", "gpu_counts"):
+        if axis in sweeps and not sweeps[axis]:
+            raise SchemaError(f"sweep axis {axis!r} must be non-empty when present")
+    cluster_path = cluster_inline = None
+    if "cluster" in data:
+        if isinstance(data["cluster"], dict):
+            cluster_inline = data["cluster"]
+        else:
+            cluster_path = str(Path(base_dir) / data["cluster"])
+    return ExperimentConfig(
+        profile_path=str(Path(base_dir) / data["profile"]),
+        cluster_path=cluster_path,
+        cluster_inline=cluster_inline,
+        schemes=tuple(data["schemes"]),
+        iterations=int(data["iterations"]),
+        partition=partition,
+        walk=walk,
+        bandwidth_scales=tuple(float(x) for x in sweeps.get("bandwidth_scale", [])),
+        partition_sizes=tuple(int(x) for x in sweeps.get("partition_size", [])),
+        gpu_counts=tuple(int(x) for x in sweeps.get("gpu_counts", [])),
+    )
+
+
+def load_experiment_config(path) -> ExperimentConfig:
+    path = Path(path)
+    try:
+        data = json.loads(path.read_text())
+    except json.JSONDecodeError as e:
+        raise SchemaError(f"{path}: invalid JSON ({e})") from e
+    return experiment_config_from_dict(data, path.parent)
+
+
+def sweep_points(cfg: ExperimentConfig) -> list[SweepPoint]:
+    """The base point plus each axis varied on its own (cli.py:160-175)."""
+    points = [SweepPoint()]
+    for s in cfg.bandwidth_scales:
+        if s != 1.0:
+            points.append(SweepPoint(bandwidth_scale=s))
+    for ps in cfg.partition_sizes:
+        if ps != cfg.partition.partition_size:
+            points.append(SweepPoint(partition_size=ps))
+    if cfg.gpu_counts:
+        ref = cfg.gpu_counts[0]
+        for g in cfg.gpu_counts[1:]:
+            points.append(SweepPoint(gpu_count=g))
+        return [p for p in points if p.gpu_count is None or p.gpu_count != ref]
+    return points
+
+
+def _ring_factor(p: int) -> float:
+    return 2.0 * (p - 1) / p
+
+
+def point_profile(profile: ModelProfile, point: SweepPoint,
+                  gpu_reference: int | None) -> ModelProfile:
+    """cli.py:178-186."""
+    factor = 1.0 / point.bandwidth_scale
+    if point.gpu_count is not None and gpu_reference:
+        factor *= _ring_factor(point.gpu_count) / _ring_factor(gpu_reference)
+    if factor == 1.0:
+        return profile
+    return profile.scaled_comm(factor, name_suffix="")
+
+
+def config_hash(cfg: ExperimentConfig, seed: int) -> str:
+    """cli.py:211-226 (same blob, so a hardware run and a simulated run of one
+    experiment file carry the same hash)."""
+    blob = json.dumps(
+        {
+            "profile": Path(cfg.profile_path).name,
+            "schemes": list(cfg.schemes),
+            "iterations": cfg.iterations,
+            "partition": vars(cfg.partition) | {},
+            "walk": vars(cfg.walk) | {} if cfg.walk else None,
+            "bandwidth_scales": list(cfg.bandwidth_scales),
+            "partition_sizes": list(cfg.partition_sizes),
+            "gpu_counts": list(cfg.gpu_counts),
+            "seed": seed,
+        },
+        sort_keys=True,
+    )
+    return hashlib.sha256(blob.encode()).hexdigest()[:16]
+
+
+# ------------------------------------------------------------ reports (simulator.py:64-300)
+
+@dataclass(frozen=True)
+class RunReport:
+    """The fields of SimReport.summary_dict (simulator.py:75-86)."""
+
+    scheme: str
+    profile_name: str
+    iterations: int
+    total_time_us: int
+    mean_iteration_time_us: float
+    bubble_time_us: int
+    bubble_ratio: float
+    updates_performed: int
+    throughput_samples_per_s: float
+
+    @classmethod
+    def from_measurement(cls, scheme: str, profile_name: str, iterations: int,
+                         total_ms: float, compute_only_ms_per_step: float,
+                         batch_size: int, updates_performed: int) -> "RunReport":
+        total_us = int(round(total_ms * 1e3))
+        bubble = max(0, total_us - int(round(compute_only_ms_per_step * 1e3 * iterations)))
+        return cls(scheme, profile_name, iterations, total_us,
+                   total_us / iterations if iterations else 0.0, bubble,
+                   bubble / total_us if total_us > 0 else 0.0, updates_performed,
+                   iterations * batch_size / (total_us / 1e6) if total_us > 0 else 0.0)
+
+    def summary_dict(self) -> dict:
+        return {
+            "scheme": self.scheme,
+            "profile": self.profile_name,
+            "iterations": self.iterations,
+            "total_time_us": self.total_time_us,
+            "mean_iteration_time_us": round(self.mean_iteration_time_us, 3),
+            "bubble_time_us": self.bubble_time_us,
+            "bubble_ratio": round(self.bubble_ratio, 6),
+            "updates_performed": self.updates_performed,
+            "throughput_samples_per_s": round(self.throughput_samples_per_s, 3),
+        }
+
+
+def compare(reports: dict[str, RunReport], baseline: str = "wfbp") -> dict:
+    """Speedups of every scheme against a named baseline (simulator.py:276-300)."""
+    if not reports:
+        raise ComparisonError("no reports to compare")
+    names = set(r.profile_name for r in reports.values())
+    iters = set(r.iterations for r in reports.values())
+    if len(iters) != 1:
+        raise ComparisonError(f"iteration counts differ: {sorted(iters)}")
+    if baseline not in reports:
+        raise ComparisonError(f"baseline {baseline!r} missing from reports")
+    base = reports[baseline].total_time_us
+    rows = []
+    for scheme in sorted(reports):
+        r = reports[scheme]
+        rows.append({
+            "scheme": scheme,
+            "profile": r.profile_name,
+            "total_time_us": r.total_time_us,
+            "mean_iteration_time_us": round(r.mean_iteration_time_us, 3),
+            "bubble_ratio": round(r.bubble_ratio, 6),
+            "updates_performed": r.updates_performed,
+            "speedup_vs_" + baseline: round(base / r.total_time_us, 4)
+            if r.total_time_us else 0.0,
+        })
+    return {"baseline": baseline, "profiles": sorted(names), "rows": rows}
+
+
+@dataclass
+class RunRecord:
+    scheme: str
+    point: SweepPoint
+    report: RunReport
+    schedule_scheme: str
+    verdict: dict | None
+    hardware: dict | None = None     # measured extras (world size, compute-only step, ...)
+
+    @property
+    def run_id(self) -> str:
+        return f"{self.scheme}__{self.point.label()}"
+
+
+@dataclass
+class ReportBundle:
+    config_hash: str
+    runs: list[RunRecord]
+    iterations: int
+    skipped: list[dict] = field(default_factory=list)
+
+    def by_point(self) -> dict[str, dict[str, RunRecord]]:
+        out: dict[str, dict[str, RunRecord]] = {}
+        for r in self.runs:
+            out.setdefault(r.point.label(), {})[r.scheme] = r
+        return out
+
+
+def _write_csv(path: Path, header: list[str], rows: list[list]) -> None:
+    with open(path, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(header)
+        w.writerows(rows)
+
+
+def emit_reports(bundle: ReportBundle, out_dir) -> list[Path]:
+    """summary.json, comparison.csv and plotdata/ in the schema of cli.py:294-391
+    (timeline / Chrome-trace files are simulator output and not written)."""
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    written: list[Path] = []
+    runs = []
+    for r in sorted(bundle.runs, key=lambda r: r.run_id):
+        doc = {
+            "run_id": r.run_id,
+            "scheme": r.scheme,
+            "sweep_point": {
+                "bandwidth_scale": r.point.bandwidth_scale,
+                "partition_size": r.point.partition_size,
+                "gpu_count": r.point.gpu_count,
+            },
+            "report": r.report.summary_dict(),
+            "preserver": r.verdict,
+        }
+        if r.hardware is not None:
+            doc["hardware"] = r.hardware
+        runs.append(doc)
+    summary = {"config_hash": bundle.config_hash, "iterations": bundle.iterations,
+               "runs": runs}
+    if bundle.skipped:
+        summary["skipped"] = bundle.skipped
+    spath = out / "summary.json"
+    spath.write_text(json.dumps(summary, indent=2, sort_keys=True) + "\n")
+    written.append(spath)
+    if not bundle.runs:
+        return written
+
+    comp_rows = []
+    for label, by_scheme in sorted(bundle.by_point().items()):
+        baseline = "wfbp" if "wfbp" in by_scheme else sorted(by_scheme)[0]
+        table = compare({s: r.report for s, r in by_scheme.items()}, baseline)
+        for row in table["rows"]:
+            comp_rows.append([label, row["scheme"], row["total_time_us"],
+                              row["mean_iteration_time_us"], row["bubble_ratio"],
+                              row["updates_performed"], row[f"speedup_vs_{baseline}"]])
+    cpath = out / "comparison.csv"
+    _write_csv(cpath, ["sweep_point", "scheme", "total_time_us", "mean_iteration_time_us",
+                       "bubble_ratio", "updates_performed", "speedup_vs_baseline"], comp_rows)
+    written.append(cpath)
+
+    plot_dir = out / "plotdata"
+    plot_dir.mkdir(exist_ok=True)
+    by_point = bundle.by_point()
+
+    def speedup_rows(points):
+        rows = []
+        for label, x in points:
+            by_scheme = by_point.get(label, {})
+            if "wfbp" not in by_scheme:
+                continue
+            base = by_scheme["wfbp"].report.total_time_us
+            for scheme in sorted(by_scheme):
+                t = by_scheme[scheme].report.total_time_us
+                rows.append([x, scheme, round(base / t, 4) if t else 0.0])
+        return rows
+
+    bw_points = [("base", 1.0)] + [
+        (SweepPoint(bandwidth_scale=s).label(), s)
+        for s in sorted({r.point.bandwidth_scale for r in bundle.runs} - {1.0})]
+    rows = speedup_rows(bw_points)
+    if rows:
+        p = plot_dir / "speedup_vs_bandwidth.csv"
+        _write_csv(p, ["bandwidth_scale", "scheme", "speedup_vs_wfbp"], rows)
+        written.append(p)
+    ps_points = [(SweepPoint(partition_size=ps).label(), ps) for ps in
+                 sorted({r.point.partition_size for r in bundle.runs if r.point.partition_size})]
+    rows = speedup_rows(ps_points)
+    if rows:
+        p = plot_dir / "speedup_vs_partition_size.csv"
+        _write_csv(p, ["partition_size", "scheme", "speedup_vs_wfbp"], rows)
+        written.append(p)
+    return written
+
+
+# ------------------------------------------------------------------- running on GPUs
+
+def preserver_verdict(schedule: Schedule, walk: WalkParams) -> dict:
+    """The verdict block of cli.py:255-266."""
+    seq = extract_batch_sequence(schedule)
+    preserved, ratio, merged, base = check_sequence(seq, walk)
+    return {"preserved": preserved, "ratio": round(ratio, 6),
+            "expected_state": round(merged, 9), "baseline_state": round(base, 9),
+            "k_values": list(seq.k_values)}
+
+
+def run_hw_experiment(cfg: ExperimentConfig, make_model: Callable, batch, loss_fn: Callable,
+                      seed: int = 0, warmup: int = 3, executor_kwargs: dict | None = None,
+                      process_group=None, log: Callable | None = None,
+                      compute_only_ms: Callable | None = None) -> ReportBundle:
+    """Run every (scheme, sweep point) of ``cfg`` on this process's GPU (one
+    process per GPU, all ranks call it).  ``make_model()`` builds a fresh
+    random-init model on the device for each run; the B200 profile is measured
+    once (CUDA events) and shared by every run, as the reference shares its
+    fixture profile.  ``compute_only_ms(model)`` times one forward+backward step
+    without communication or update (default: eager, under the executor's
+    autocast).  Returns the bundle (``emit_reports`` writes it)."""
+    import torch
+
+    from .executor import DeftConfig, DeftDataParallel
+
+    import contextlib
+    import gc
+
+    dist = torch.distributed
+    ac_dtype = (executor_kwargs or {}).get("autocast_dtype", torch.bfloat16)
+
+    def autocast():
+        if ac_dtype is None:
+            return contextlib.nullcontext()
+        return torch.autocast("cuda", dtype=ac_dtype)
+
+    world = dist.get_world_size(process_group) if dist.is_initialized() else 1
+    kw = dict(executor_kwargs or {})
+
+    def executor(scheme, partition):
+        model = make_model()
+        dcfg = DeftConfig(scheme="deft" if scheme.startswith("deft") else scheme,
+                          partition=partition, **kw)
+        return model, DeftDataParallel(model, dcfg, process_group=process_group)
+
+    def timed_steps(ddp, model, n):
+        if world > 1:
+            dist.barrier(group=process_group)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(n):
+            if ddp is None:
+                model.zero_grad(set_to_none=True)
+                with autocast():
+                    loss = loss_fn(model, batch)
+                loss.backward()
+            else:
+                ddp.train_step(batch, loss_fn)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([ms], device=torch.device("cuda", torch.cuda.current_device()))
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=process_group)
+            ms = float(t.item())
+        return ms
+
+    # the profile of THIS hardware, measured once
+    model, ddp = executor("deft", cfg.partition)
+    profile = ddp.measure_profile(batch, loss_fn, iters=3,
+                                  name=Path(cfg.profile_path).stem,
+                                  batch_size=int(batch[0].shape[0]))
+    cluster = ddp.cluster
+    ddp.close()
+    # compute-only step (forward + backward, no communication, no update)
+    model = make_model()
+    if compute_only_ms is not None:
+        compute_ms = compute_only_ms(model)
+    else:
+        timed_steps(None, model, warmup)
+        compute_ms = timed_steps(None, model, cfg.iterations) / cfg.iterations
+    del model
+
+    gpu_ref = cfg.gpu_counts[0] if cfg.gpu_counts else None
+    runs, skipped = [], []
+    for point in sweep_points(cfg):
+        if point.gpu_count is not None and point.gpu_count != world:
+            skipped.append({"sweep_point": point.label(),
+                            "reason": f"launched on {world} GPU(s)"})
+            continue
+        p_profile = point_profile(profile, point, gpu_ref)
+        p_partition = cfg.partition
+        if point.partition_size is not None:
+            p_partition = replace(cfg.partition, partition_size=point.partition_size)
+        for scheme in cfg.schemes:
+            if scheme not in HW_SCHEMES:
+                skipped.append({"sweep_point": point.label(), "scheme": scheme,
+                                "reason": "simulator-scored baseline, not an executor "
+                                          "schedule (DESIGN.md §7)"})
+                continue
+            model, ddp = executor(scheme, p_partition)
+            links = (ClusterSpec(links=(cluster.fast_link,))
+                     if scheme == "deft_single_link" else cluster)
+            part = ddp.plan(p_profile, links)
+            ddp.warm_up(batch, loss_fn, min_steps=warmup)
+            u0 = ddp.updates_applied
+            total_ms = timed_steps(ddp, model, cfg.iterations)
+            updates = ddp.updates_applied - u0
+            verdict = None
+            if scheme.startswith("deft") and cfg.walk is not None:
+                decisions = [d for pair in ddp.decision_log[:cfg.iterations] for d in pair]
+                verdict = preserver_verdict(
+                    Schedule(scheme, part, links, decisions, True, cfg.iterations), cfg.walk)
+            report = RunReport.from_measurement(
+                scheme, profile.name, cfg.iterations, total_ms, compute_ms,
+                profile.batch_size, updates)
+            runs.append(RunRecord(scheme, point, report, scheme, verdict, hardware={
+                "world": world, "buckets": part.n_buckets,
+                "links": [l.name for l in links.links],
+                "compute_only_ms_per_step": round(compute_ms, 4),
+                "global_samples_per_s": round(report.throughput_samples_per_s * world, 2),
+                "update_placement": ddp.placement,
+                "graph_choice": ddp.graph_choice}))
+            if log is not None:
+                log(runs[-1])
+            ddp.close()
+            del model, ddp
+            gc.collect()                  # captured graphs and their pools
+            torch.cuda.empty_cache()
+    return ReportBundle(config_hash(cfg, seed), runs, cfg.iterations, skipped)
