@@ -136,6 +136,8 @@ class DeftDataParallel:
         self.compute_stream = torch.cuda.Stream(self.device)
         prio_lo, prio_hi = torch.cuda.Stream.priority_range()
         self.update_stream = torch.cuda.Stream(self.device, priority=prio_hi)
+        # store path: bucket gathers run here, off the backward's critical path
+        self.gather_stream = torch.cuda.Stream(self.device)
         self.link_streams: list[torch.cuda.Stream] = []
         self.profile: ModelProfile | None = None
         self.schedule_profile: ModelProfile | None = None
@@ -505,16 +507,19 @@ class DeftDataParallel:
 
     def _start_groups(self) -> list[list[int]]:
         """Consecutive buckets in forward order (input side first) coalesced into at
-        most `start_groups` groups of similar size: one update launch per group."""
+        most `start_groups` groups whose sizes double: the forward's first modules
+        wait only for a small first update, and each later (larger) group's update
+        runs while the forward works through the groups before it.  One update
+        launch per group."""
         if getattr(self, "_groups_cache", None) is None:
             order = list(range(len(self.buckets) - 1, -1, -1))
             n_groups = max(1, min(self.cfg.start_groups, len(order)))
-            target = self.total / n_groups
+            unit = self.total / (2 ** n_groups - 1)
             groups, cur, acc = [], [], 0
             for b in order:
                 cur.append(b)
                 acc += self.buckets[b].hi - self.buckets[b].lo
-                if acc >= target * (len(groups) + 1) and len(groups) < n_groups - 1:
+                if acc >= unit * (2 ** (len(groups) + 1) - 1) and len(groups) < n_groups - 1:
                     groups.append(cur)
                     cur = []
             if cur:
@@ -604,10 +609,19 @@ class DeftDataParallel:
             self.comm.gather(slot, srcs, offs, lens, stream)
 
     def _bucket_ready(self, bidx: int):
-        if self._gather_slot is not None:
-            self._gather_bucket(bidx, self._gather_slot)
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))
+        if self._gather_slot is not None:
+            # copy the fresh gradients into the slot on the gather stream: the
+            # backward continues while they move (the compute stream joins it
+            # once, after the whole backward); the bucket's transfers wait for it
+            gs = self.gather_stream
+            gs.wait_event(ev)
+            self._touched[id(gs)] = gs
+            with torch.cuda.stream(gs):
+                self._gather_bucket(bidx, self._gather_slot)
+            ev = torch.cuda.Event()
+            ev.record(gs)
         for link, slot in self._fresh_now.pop(bidx, ()):
             self._issue_rs(link, slot, bidx, ev)
         if self.placement == "bucket":
@@ -663,6 +677,10 @@ class DeftDataParallel:
         for b in range(len(self.buckets)):      # buckets whose params got no gradient
             if not self._fired[b]:
                 self._bucket_ready(b)
+        if self._gather_slot is not None:
+            # every gather done before the slot is read by an update on this
+            # stream and before autograd's gradient buffers can be reused
+            comp.wait_stream(self.gather_stream)
         if self.placement == "end" and self._due_now:
             self._updates_at_end(comp)
         if self._fresh_now:
