@@ -156,6 +156,14 @@ deft_status_t deft_comm_set_update_blocks(deft_comm* c, int32_t blocks);
 deft_status_t deft_bucket_reduce_scatter(deft_comm* c, int32_t channel, int32_t slot,
                                          int64_t offset, int64_t numel, void* stream);
 
+/* The transfers one release point puts on one link (simulator.py:184-196: a
+ * forward/backward-stage plan, or the fresh buckets that become ready at the
+ * same backward moment) in ONE launch with one cross-rank barrier: the same
+ * result as `count` deft_bucket_reduce_scatter calls in list order. */
+deft_status_t deft_bucket_reduce_scatter_multi(deft_comm* c, int32_t channel, int32_t slot,
+                                               int32_t count, const int64_t* offsets,
+                                               const int64_t* numels, void* stream);
+
 /* Fused delayed SGD/momentum update of the owned shard + all-gather of the
  * updated parameters to every rank (the update event, scheduler.py:56-61):
  *   g = shard(slot) * grad_scale          (grad_scale = 1 / (W * merge_count))

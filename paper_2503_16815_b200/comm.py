@@ -118,6 +118,16 @@ class BucketComm:
                                                        c_vp(stream.cuda_stream)),
               "deft_bucket_reduce_scatter")
 
+    def reduce_scatter_multi(self, channel: int, slot: int, ranges, stream) -> None:
+        """Buckets released together on one link, one launch / one barrier
+        (deft_bucket_reduce_scatter_multi); ``ranges`` = [(lo, hi), ...] in plan order."""
+        n = len(ranges)
+        offs = (ctypes.c_int64 * n)(*[lo for lo, _ in ranges])
+        lens = (ctypes.c_int64 * n)(*[hi - lo for lo, hi in ranges])
+        check(_native.lib().deft_bucket_reduce_scatter_multi(
+            self._h, channel, slot, n, offs, lens, c_vp(stream.cuda_stream)),
+            "deft_bucket_reduce_scatter_multi")
+
     def set_update_blocks(self, blocks: int) -> None:
         """CTA budget of the update kernels (0 = default); identical on every rank."""
         check(_native.lib().deft_comm_set_update_blocks(self._h, int(blocks)),

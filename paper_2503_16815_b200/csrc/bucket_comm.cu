@@ -26,6 +26,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace deft {
@@ -271,6 +273,25 @@ static void rs_dispatch(int world, int grid, cudaStream_t stream, const PeerPtrs
 bool launch_reduce_scatter_tma(const PeerPtrs& P, int rank, int world, int dtype,
                                int64_t slot_base, int64_t offset, int64_t numel,
                                cudaStream_t stream);
+
+bool launch_reduce_scatter_tma_multi(const PeerPtrs& P, int rank, int world, int dtype,
+                                     int64_t slot_base, int32_t count, const int64_t* offsets,
+                                     const int64_t* numels, cudaStream_t stream);
+
+cudaError_t launch_reduce_scatter_sm_multi(const PeerPtrs& P, int rank, int world, int dtype,
+                                           int64_t slot_base, int32_t count,
+                                           const int64_t* offsets, const int64_t* numels,
+                                           cudaStream_t stream) {
+  if (launch_reduce_scatter_tma_multi(P, rank, world, dtype, slot_base, count, offsets, numels,
+                                      stream))
+    return cudaGetLastError();
+  for (int32_t k = 0; k < count; ++k) {   // LDG kernel: one launch per bucket
+    cudaError_t e = launch_reduce_scatter_sm(P, rank, world, dtype, slot_base, offsets[k],
+                                             numels[k], stream);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
 
 cudaError_t launch_reduce_scatter_sm(const PeerPtrs& P, int rank, int world, int dtype,
                                      int64_t slot_base, int64_t offset, int64_t numel,
@@ -607,17 +628,42 @@ __global__ void __launch_bounds__(kLocalThreads) gather_kernel(char* __restrict_
 }  // namespace deft
 
 namespace deft {
+// Segments of at least this many bytes are copied by the copy engines
+// (cudaMemcpyAsync D2D: no SMs, so the concurrent backward keeps all of them);
+// the rest by gather_kernel.  DEFT_GATHER_CE_MIN (bytes; 0 = kernel only).
+static int64_t gather_ce_min() {
+  static int64_t v = [] {
+    const char* e = getenv("DEFT_GATHER_CE_MIN");
+    return e ? (int64_t)atoll(e) : (int64_t)(4 << 20);
+  }();
+  return v;
+}
+
 cudaError_t launch_gather(char* dst, const void* const* srcs, const int64_t* dst_off,
                           const int64_t* lens, int32_t count, cudaStream_t stream) {
-  for (int32_t s0 = 0; s0 < count; s0 += kMaxGatherSeg) {
+  const int64_t ce_min = gather_ce_min();
+  std::vector<int32_t> small;
+  small.reserve(count);
+  for (int32_t k = 0; k < count; ++k) {
+    if (ce_min > 0 && lens[k] >= ce_min) {
+      cudaError_t e = cudaMemcpyAsync(dst + dst_off[k], srcs[k], (size_t)lens[k],
+                                      cudaMemcpyDeviceToDevice, stream);
+      if (e != cudaSuccess) return e;
+    } else if (lens[k] > 0) {
+      small.push_back(k);
+    }
+  }
+  const int32_t n_small = (int32_t)small.size();
+  for (int32_t s0 = 0; s0 < n_small; s0 += kMaxGatherSeg) {
     GatherTable t;
-    t.count = count - s0 < kMaxGatherSeg ? count - s0 : kMaxGatherSeg;
+    t.count = n_small - s0 < kMaxGatherSeg ? n_small - s0 : kMaxGatherSeg;
     t.first[0] = 0;
     for (int k = 0; k < t.count; ++k) {
-      t.src[k] = reinterpret_cast<const char*>(srcs[s0 + k]);
-      t.dst_off[k] = dst_off[s0 + k];
-      t.len[k] = lens[s0 + k];
-      t.first[k + 1] = t.first[k] + (lens[s0 + k] + 15) / 16;
+      const int32_t i = small[s0 + k];
+      t.src[k] = reinterpret_cast<const char*>(srcs[i]);
+      t.dst_off[k] = dst_off[i];
+      t.len[k] = lens[i];
+      t.first[k + 1] = t.first[k] + (lens[i] + 15) / 16;
     }
     const int64_t total = t.first[t.count];
     if (total == 0) continue;
@@ -802,38 +848,86 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem
       : "memory");
 }
 
+struct ChunkTable {           // this rank's owned shards, cut into TMA chunks
+  int64_t off[kMaxSeg];       // aligned body start of each segment
+  int64_t len[kMaxSeg];       // aligned body length (multiple of 8 elements)
+  int64_t first[kMaxSeg + 1]; // prefix of chunks per segment
+  int64_t head_lo[kMaxSeg], head_hi[kMaxSeg], tail_lo[kMaxSeg], tail_hi[kMaxSeg];
+  int32_t count;
+};
+
+// Segments [s0, s0 + t.count) of a bucket list -> this rank's shard of each
+// (shard_of: the same ownership every comm kernel uses), 8-element-aligned
+// bodies cut into `chunk`-element pieces, unaligned heads/tails apart.
+// Returns the number of owned elements.
+static int64_t build_chunk_table(ChunkTable& t, int32_t s0, int32_t count,
+                                 const int64_t* offsets, const int64_t* numels, int rank,
+                                 int world, int align, int64_t chunk) {
+  t.count = count - s0 < kMaxSeg ? count - s0 : kMaxSeg;
+  t.first[0] = 0;
+  int64_t owned = 0;
+  for (int k = 0; k < t.count; ++k) {
+    const ShardRange sh = shard_of(offsets[s0 + k], numels[s0 + k], rank, world, align);
+    int64_t a = (sh.lo + 7) / 8 * 8;
+    if (a > sh.hi) a = sh.hi;
+    int64_t b = sh.hi / 8 * 8;
+    if (b < a) b = a;
+    t.head_lo[k] = sh.lo; t.head_hi[k] = a;
+    t.tail_lo[k] = b; t.tail_hi[k] = sh.hi;
+    t.off[k] = a;
+    t.len[k] = b - a;
+    t.first[k + 1] = t.first[k] + (t.len[k] + chunk - 1) / chunk;
+    owned += sh.hi - sh.lo;
+  }
+  return owned;
+}
+
+__device__ __forceinline__ void table_chunk(const ChunkTable& t, int64_t chunk, int64_t c,
+                                            int64_t* e0, int64_t* len) {
+  int sgi = 0;
+  while (c >= t.first[sgi + 1]) ++sgi;
+  *e0 = t.off[sgi] + (c - t.first[sgi]) * chunk;
+  const int64_t rem = t.off[sgi] + t.len[sgi] - *e0;
+  *len = rem < chunk ? rem : chunk;
+}
+
+template <typename T, int W>
+__host__ __device__ constexpr int64_t rs_tma_chunk() {  // elements per peer chunk
+  return (kTmaStageBytes / W / (int)sizeof(T)) / 8 * 8;
+}
+
+// One launch reduces every segment of the table (all buckets released together
+// on this link): one entry barrier instead of one per bucket.
 template <typename T, int W>
 __global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
-    PeerPtrs P, int rank, int64_t slot_base, int64_t lo, int64_t hi) {
+    PeerPtrs P, int rank, int64_t slot_base, ChunkTable t) {
   using V = Vec<T>;
   extern __shared__ __align__(128) unsigned char tma_smem[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   // elements per peer chunk: a stage holds W chunks, 16-byte granular
-  constexpr int64_t kChunk = (kTmaStageBytes / W / (int)sizeof(T)) / 8 * 8;
+  constexpr int64_t kChunk = rs_tma_chunk<T, W>();
   const uint32_t epoch = take_epochs(P, rank, kBarrierRS, 1u) + 1u;
   peer_block_barrier(P, rank, W, kBarrierRS, blockIdx.x, epoch);
   const T* src[W];
 #pragma unroll
   for (int k = 0; k < W; ++k) src[k] = reinterpret_cast<const T*>(P.grads[k]) + slot_base;
   T* dst = reinterpret_cast<T*>(P.grads[rank]) + slot_base;
-  const Span s = split_span<V::N>(lo, hi);
-  if (blockIdx.x == 0) {  // unaligned edges
-    for (int64_t e = s.head_lo + threadIdx.x; e < s.head_hi; e += blockDim.x) {
-      float acc = 0.f;
+  if (blockIdx.x == 0) {  // unaligned edges of every segment
+    for (int sgi = 0; sgi < t.count; ++sgi) {
+      for (int part = 0; part < 2; ++part) {
+        const int64_t a = part ? t.tail_lo[sgi] : t.head_lo[sgi];
+        const int64_t b = part ? t.tail_hi[sgi] : t.head_hi[sgi];
+        for (int64_t e = a + threadIdx.x; e < b; e += blockDim.x) {
+          float acc = 0.f;
 #pragma unroll
-      for (int k = 0; k < W; ++k) acc += V::scalar(src[k] + e);
-      V::put(dst + e, acc);
-    }
-    for (int64_t e = s.tail_lo + threadIdx.x; e < s.tail_hi; e += blockDim.x) {
-      float acc = 0.f;
-#pragma unroll
-      for (int k = 0; k < W; ++k) acc += V::scalar(src[k] + e);
-      V::put(dst + e, acc);
+          for (int k = 0; k < W; ++k) acc += V::scalar(src[k] + e);
+          V::put(dst + e, acc);
+        }
+      }
     }
   }
-  // this CTA's contiguous share of the aligned body, in chunks
-  const int64_t body = s.body_hi - s.body_lo;
-  const int64_t n_chunks = (body + kChunk - 1) / kChunk;
+  // this CTA's contiguous share of the table's chunks
+  const int64_t n_chunks = t.first[t.count];
   const int64_t c_begin = n_chunks * blockIdx.x / gridDim.x;
   const int64_t c_end = n_chunks * (blockIdx.x + 1) / gridDim.x;
   if (threadIdx.x == 0) {
@@ -846,8 +940,8 @@ __global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
   };
   auto issue = [&](int64_t c) {  // one elected thread: W bulk copies of chunk c
     const int st = (int)((c - c_begin) % kTmaStages);
-    const int64_t e0 = s.body_lo + c * kChunk;
-    const int64_t len = min(kChunk, s.body_hi - e0);
+    int64_t e0, len;
+    table_chunk(t, kChunk, c, &e0, &len);
     const uint32_t bytes = (uint32_t)(len * sizeof(T));
     // the stage was last read through the generic proxy; order that before the
     // async-proxy (TMA) writes that refill it
@@ -864,8 +958,8 @@ __global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
     // keep the ring full: chunk c + S - 1 goes into the stage freed at the end of c - 1
     if (threadIdx.x == 0 && c + kTmaStages - 1 < c_end) issue(c + kTmaStages - 1);
     mbar_wait(&full[st], parity);
-    const int64_t e0 = s.body_lo + c * kChunk;
-    const int64_t len = min(kChunk, s.body_hi - e0);
+    int64_t e0, len;
+    table_chunk(t, kChunk, c, &e0, &len);
     using Raw = typename V::Raw;
     for (int64_t v = threadIdx.x; v < len / V::N; v += blockDim.x) {
       float acc[V::N], tmp[V::N];
@@ -884,7 +978,7 @@ __global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
 
 template <typename T>
 static void rs_tma_dispatch(int world, int grid, cudaStream_t stream, const PeerPtrs& P,
-                            int rank, int64_t slot_base, int64_t lo, int64_t hi) {
+                            int rank, int64_t slot_base, const ChunkTable& t) {
   const size_t smem = (size_t)kTmaStages * kTmaStageBytes;
 #define DEFT_RST_CASE(WW)                                                                      \
   case WW: {                                                                                   \
@@ -895,7 +989,7 @@ static void rs_tma_dispatch(int world, int grid, cudaStream_t stream, const Peer
       attr = true;                                                                             \
     }                                                                                          \
     reduce_scatter_tma_kernel<T, WW><<<grid, kTmaThreads, smem, stream>>>(P, rank, slot_base,  \
-                                                                          lo, hi);             \
+                                                                          t);                  \
     break;                                                                                     \
   }
   switch (world) {
@@ -925,21 +1019,37 @@ static int rs_tma_blocks() {
   return v;
 }
 
+static int64_t rs_chunk_for(int world, int dtype) {
+  const int esz = dtype == 0 ? 4 : 2;
+  return (kTmaStageBytes / world / esz) / 8 * 8;   // == rs_tma_chunk<T, W>()
+}
+
+bool launch_reduce_scatter_tma_multi(const PeerPtrs& P, int rank, int world, int dtype,
+                                     int64_t slot_base, int32_t count, const int64_t* offsets,
+                                     const int64_t* numels, cudaStream_t stream) {
+  if (!rs_impl_tma() || world < 2 || world > 8) return false;
+  const int align = dtype == 0 ? 4 : 8;
+  for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
+    ChunkTable t{};
+    const int64_t owned = build_chunk_table(t, s0, count, offsets, numels, rank, world, align,
+                                            rs_chunk_for(world, dtype));
+    int grid = (int)((owned + 32767) / 32768);
+    if (grid < 1) grid = 1;
+    if (grid > rs_tma_blocks()) grid = rs_tma_blocks();
+    if (dtype == 0)
+      rs_tma_dispatch<float>(world, grid, stream, P, rank, slot_base, t);
+    else
+      rs_tma_dispatch<__nv_bfloat16>(world, grid, stream, P, rank, slot_base, t);
+    count_launch();
+  }
+  return true;
+}
+
 bool launch_reduce_scatter_tma(const PeerPtrs& P, int rank, int world, int dtype,
                                int64_t slot_base, int64_t offset, int64_t numel,
                                cudaStream_t stream) {
-  if (!rs_impl_tma()) return false;
-  const ShardRange sh = shard_of(offset, numel, rank, world, dtype == 0 ? 4 : 8);
-  const int64_t per = (numel + world - 1) / world;
-  int grid = (int)((per + 32767) / 32768);
-  if (grid < 1) grid = 1;
-  if (grid > rs_tma_blocks()) grid = rs_tma_blocks();
-  if (dtype == 0)
-    rs_tma_dispatch<float>(world, grid, stream, P, rank, slot_base, sh.lo, sh.hi);
-  else
-    rs_tma_dispatch<__nv_bfloat16>(world, grid, stream, P, rank, slot_base, sh.lo, sh.hi);
-  count_launch();
-  return true;
+  return launch_reduce_scatter_tma_multi(P, rank, world, dtype, slot_base, 1, &offset, &numel,
+                                         stream);
 }
 
 }  // namespace deft
@@ -976,13 +1086,6 @@ __device__ __forceinline__ void tma_store_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-struct ChunkTable {           // this rank's owned shards, cut into TMA chunks
-  int64_t off[kMaxSeg];       // aligned body start of each segment
-  int64_t len[kMaxSeg];       // aligned body length (multiple of 8 elements)
-  int64_t first[kMaxSeg + 1]; // prefix of chunks per segment
-  int64_t head_lo[kMaxSeg], head_hi[kMaxSeg], tail_lo[kMaxSeg], tail_hi[kMaxSeg];
-  int32_t count;
-};
 
 template <typename T, int W>
 __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
@@ -1031,12 +1134,7 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
   }
   __syncthreads();
   auto chunk_range = [&](int64_t c, int64_t* e0, int64_t* len) {
-    int sgi = 0;
-    while (c >= t.first[sgi + 1]) ++sgi;
-    const int64_t k = c - t.first[sgi];
-    *e0 = t.off[sgi] + k * kUpdChunk;
-    const int64_t rem = t.off[sgi] + t.len[sgi] - *e0;
-    *len = rem < kUpdChunk ? rem : kUpdChunk;
+    table_chunk(t, kUpdChunk, c, e0, len);
   };
   auto base = [&](int st) { return usmem + (size_t)st * kStage; };
   auto issue_load = [&](int64_t c) {
@@ -1117,22 +1215,9 @@ bool launch_update_allgather_tma(const PeerPtrs& P, int rank, int world, int dty
   const int align = dtype == 0 ? 4 : 8;
   for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
     ChunkTable t{};
-    t.count = count - s0 < kMaxSeg ? count - s0 : kMaxSeg;
-    t.first[0] = 0;
+    build_chunk_table(t, s0, count, offsets, numels, rank, world, align, kUpdChunk);
     int64_t total_elems = 0;
-    for (int k = 0; k < t.count; ++k) {
-      const ShardRange sh = shard_of(offsets[s0 + k], numels[s0 + k], rank, world, align);
-      int64_t a = (sh.lo + 7) / 8 * 8;
-      if (a > sh.hi) a = sh.hi;
-      int64_t b = sh.hi / 8 * 8;
-      if (b < a) b = a;
-      t.head_lo[k] = sh.lo; t.head_hi[k] = a;
-      t.tail_lo[k] = b; t.tail_hi[k] = sh.hi;
-      t.off[k] = a;
-      t.len[k] = b - a;
-      t.first[k + 1] = t.first[k] + (t.len[k] + kUpdChunk - 1) / kUpdChunk;
-      total_elems += numels[s0 + k];
-    }
+    for (int k = 0; k < t.count; ++k) total_elems += numels[s0 + k];
     int grid = comm_grid_for((total_elems + world - 1) / world);
     if (max_blocks > 0 && grid > max_blocks) grid = max_blocks;
     const size_t esz = dtype == 0 ? 4 : 2;

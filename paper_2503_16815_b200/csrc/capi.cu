@@ -428,6 +428,69 @@ extern "C" deft_status_t deft_bucket_reduce_scatter(deft_comm* c, int32_t channe
   return DEFT_OK;
 }
 
+extern "C" deft_status_t deft_bucket_reduce_scatter_multi(deft_comm* c, int32_t channel,
+                                                          int32_t slot, int32_t count,
+                                                          const int64_t* offsets,
+                                                          const int64_t* numels, void* stream) {
+  if (!c) return fail(DEFT_ERR_INVALID_ARGUMENT, "null comm");
+  if (count < 0 || (count > 0 && (!offsets || !numels)))
+    return fail(DEFT_ERR_INVALID_ARGUMENT, "bad bucket list");
+  for (int32_t k = 0; k < count; ++k) {
+    deft_status_t st = check_range(c, slot, offsets[k], numels[k]);
+    if (st != DEFT_OK) return st;
+  }
+  if (c->world == 1 || count == 0) return DEFT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t slot_base = (int64_t)slot * c->slot_elems;
+  if (channel == DEFT_CHANNEL_SM) {
+    cudaError_t e = launch_reduce_scatter_sm_multi(c->P, c->rank, c->world, c->dtype, slot_base,
+                                                   count, offsets, numels, s);
+    if (e != cudaSuccess) return cuda_fail(e, "reduce_scatter_tma_kernel");
+    return DEFT_OK;
+  }
+  if (channel != DEFT_CHANNEL_CE) return fail(DEFT_ERR_INVALID_ARGUMENT, "bad channel");
+  // copy-engine channel: ONE barrier, then per bucket (W-1) DMA copies + local reduce
+  const int esz = c->dtype == DEFT_DTYPE_F32 ? 4 : 2;
+  size_t need = 0;
+  for (int32_t k = 0; k < count; ++k) {
+    const int64_t per = ((numels[k] + c->world - 1) / c->world + 16 + 7) / 8 * 8;
+    need += (size_t)(c->world - 1) * per * esz;
+  }
+  if (need > c->staging_bytes) {
+    if (c->staging) {
+      DEFT_CUDA(cudaStreamSynchronize(s));
+      cudaFree(c->staging);
+    }
+    DEFT_CUDA(cudaMalloc(&c->staging, need));
+    c->staging_bytes = need;
+  }
+  cudaError_t e = launch_barrier(c->P, c->rank, c->world, kBarrierCE, s);
+  if (e != cudaSuccess) return cuda_fail(e, "barrier_kernel");
+  size_t base = 0;
+  for (int32_t k = 0; k < count; ++k) {
+    const ShardRange sh = shard_of(offsets[k], numels[k], c->rank, c->world,
+                                   c->dtype == 0 ? 4 : 8);
+    const int64_t len = sh.hi - sh.lo;
+    const int64_t per = ((numels[k] + c->world - 1) / c->world + 16 + 7) / 8 * 8;
+    char* stage = c->staging + base;
+    if (len > 0) {
+      int j = 0;
+      for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) continue;
+        const char* src = c->P.grads[r] + (slot_base + sh.lo) * esz;
+        DEFT_CUDA(cudaMemcpyAsync(stage + (size_t)j * per * esz, src, (size_t)len * esz,
+                                  cudaMemcpyDeviceToDevice, s));
+        ++j;
+      }
+      e = launch_ce_reduce(c->P.grads[c->rank] + slot_base * esz, stage, c->dtype, c->world,
+                           c->rank, sh.lo, len, per, s);
+      if (e != cudaSuccess) return cuda_fail(e, "ce_reduce_kernel");
+    }
+    base += (size_t)(c->world - 1) * per * esz;
+  }
+  return DEFT_OK;
+}
+
 extern "C" deft_status_t deft_bucket_update(deft_comm* c, int32_t slot, int64_t offset,
                                            int64_t numel, float lr, float momentum,
                                            float grad_scale, float* d_mom, void* stream) {

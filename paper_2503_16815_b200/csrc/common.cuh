@@ -70,6 +70,10 @@ int comm_grid_for(int64_t elems_per_rank);
 cudaError_t launch_reduce_scatter_sm(const PeerPtrs& P, int rank, int world, int dtype,
                                      int64_t slot_base, int64_t offset, int64_t numel,
                                      cudaStream_t stream);
+cudaError_t launch_reduce_scatter_sm_multi(const PeerPtrs& P, int rank, int world, int dtype,
+                                           int64_t slot_base, int32_t count,
+                                           const int64_t* offsets, const int64_t* numels,
+                                           cudaStream_t stream);
 cudaError_t launch_barrier(const PeerPtrs& P, int rank, int world, int set,
                            cudaStream_t stream);
 cudaError_t launch_ce_reduce(char* own_grad_slot, const char* staging, int dtype, int world,

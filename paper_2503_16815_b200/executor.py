@@ -444,24 +444,43 @@ class DeftDataParallel:
         b.record(stream)
         self._events_t.append((kind, a, b, nbytes))
 
-    def _issue_rs(self, link: int, slot: int, bidx: int, release: torch.cuda.Event):
-        if self.world == 1:
+    def _issue_rs(self, link: int, slot: int, bidxs: list[int], release: torch.cuda.Event):
+        """The buckets one release point puts on one link, in plan order: ONE
+        reduce-scatter launch (one cross-rank barrier) on the link's stream."""
+        if self.world == 1 or not bidxs:
             return
-        b = self.buckets[bidx]
         s = self.link_streams[link]
         s.wait_event(release)
         self._touched[id(s)] = s
         esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
-        nbytes = (b.hi - b.lo) * esz * (self.world - 1) // self.world  # crossing NVLink
+        ranges = [(self.buckets[b].lo, self.buckets[b].hi) for b in bidxs]
+        elems = sum(hi - lo for lo, hi in ranges)
+        nbytes = elems * esz * (self.world - 1) // self.world  # crossing NVLink
         self._timed("reduce_scatter", s,
-                    lambda: self.comm.reduce_scatter(self.channel_of_link[link], slot, b.lo,
-                                                     b.hi - b.lo, s), nbytes)
+                    lambda: self.comm.reduce_scatter_multi(self.channel_of_link[link], slot,
+                                                           ranges, s), nbytes)
         if not self._sequential or self.planner.lag == 0:
             # an update waits for it: always when streams run ahead (eager, async),
             # and within the iteration for synchronous schedules (lag 0)
             ev = torch.cuda.Event()
             ev.record(s)
-            self._rs_done[(slot, bidx)] = ev
+            for b in bidxs:
+                self._rs_done[(slot, b)] = ev
+
+    def _issue_planned(self, transfers, release: torch.cuda.Event):
+        """Stage-plan transfers (link, slot, bucket) released together: per link,
+        consecutive same-slot runs in plan order become one launch each."""
+        runs: dict[int, tuple[int, list[int]]] = {}
+        for link, slot, bidx in transfers:
+            cur = runs.get(link)
+            if cur is not None and cur[0] != slot:
+                self._issue_rs(link, cur[0], cur[1], release)
+                cur = None
+            if cur is None:
+                cur = runs[link] = (slot, [])
+            cur[1].append(bidx)
+        for link, (slot, bl) in runs.items():
+            self._issue_rs(link, slot, bl, release)
 
     def _issue_update(self, slot: int, k: int, bidx: int, window_open: torch.cuda.Event):
         b = self.buckets[bidx]
@@ -507,19 +526,19 @@ class DeftDataParallel:
 
     def _start_groups(self) -> list[list[int]]:
         """Consecutive buckets in forward order (input side first) coalesced into at
-        most `start_groups` groups whose sizes double: the forward's first modules
-        wait only for a small first update, and each later (larger) group's update
-        runs while the forward works through the groups before it.  One update
+        most `start_groups` update launches: a small first group (the forward's
+        first modules wait only for it), then groups of similar size.  One update
         launch per group."""
         if getattr(self, "_groups_cache", None) is None:
             order = list(range(len(self.buckets) - 1, -1, -1))
             n_groups = max(1, min(self.cfg.start_groups, len(order)))
-            unit = self.total / (2 ** n_groups - 1)
+            first = self.total / (4 * n_groups)
+            step = (self.total - first) / max(1, n_groups - 1)
             groups, cur, acc = [], [], 0
             for b in order:
                 cur.append(b)
                 acc += self.buckets[b].hi - self.buckets[b].lo
-                if acc >= unit * (2 ** (len(groups) + 1) - 1) and len(groups) < n_groups - 1:
+                if acc >= first + step * len(groups) and len(groups) < n_groups - 1:
                     groups.append(cur)
                     cur = []
             if cur:
@@ -580,54 +599,71 @@ class DeftDataParallel:
         if not self._in_step:
             return
         idx = self._param_index[id(p)]
+        ready = []
         for b in self._param_buckets[idx]:
             self._pending[b] -= 1
             if self._pending[b] == 0:
-                self._bucket_ready(b)
+                ready.append(b)
+        if ready:   # e.g. every piece of a partitioned layer at once
+            self._buckets_ready(ready)
 
-    def _gather_bucket(self, bidx: int, slot: int):
-        """Copy the bucket's fresh per-parameter gradients into its slot range."""
-        b = self.buckets[bidx]
+    def _gather_buckets(self, bidxs: list[int], slot: int):
+        """Copy the buckets' fresh per-parameter gradients into their slot ranges
+        (one gather launch)."""
         esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
         srcs, offs, lens = [], [], []
-        for i in self._bucket_params[bidx]:
-            p, o = self.params[i], self.offsets[i]
-            lo, hi = max(b.lo, o), min(b.hi, o + p.numel())
-            g = p.grad
-            if g is None or g.stride() != p.stride() or g.dtype != p.dtype:
-                view = self.comm.grads[slot][lo:hi]
-                if g is None:
-                    view.zero_()
-                else:
-                    self._grad_views[slot][i].copy_(g)
-                continue
-            srcs.append(g.data_ptr() + (lo - o) * esz)
-            offs.append(lo * esz)
-            lens.append((hi - lo) * esz)
+        for bidx in bidxs:
+            b = self.buckets[bidx]
+            for i in self._bucket_params[bidx]:
+                p, o = self.params[i], self.offsets[i]
+                lo, hi = max(b.lo, o), min(b.hi, o + p.numel())
+                g = p.grad
+                if g is None or g.stride() != p.stride() or g.dtype != p.dtype:
+                    view = self.comm.grads[slot][lo:hi]
+                    if g is None:
+                        view.zero_()
+                    else:   # layout differs: a strided copy of the whole parameter
+                        self._grad_views[slot][i].copy_(g)
+                    continue
+                srcs.append(g.data_ptr() + (lo - o) * esz)
+                offs.append(lo * esz)
+                lens.append((hi - lo) * esz)
         if srcs:
             stream = torch.cuda.current_stream(self.device)
             self.comm.gather(slot, srcs, offs, lens, stream)
 
-    def _bucket_ready(self, bidx: int):
+    def _buckets_ready(self, bidxs: list[int]):
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))
         if self._gather_slot is not None:
             # copy the fresh gradients into the slot on the gather stream: the
             # backward continues while they move (the compute stream joins it
-            # once, after the whole backward); the bucket's transfers wait for it
+            # once, after the whole backward); the buckets' transfers wait for it
             gs = self.gather_stream
             gs.wait_event(ev)
             self._touched[id(gs)] = gs
             with torch.cuda.stream(gs):
-                self._gather_bucket(bidx, self._gather_slot)
+                self._gather_buckets(bidxs, self._gather_slot)
             ev = torch.cuda.Event()
             ev.record(gs)
-        for link, slot in self._fresh_now.pop(bidx, ()):
-            self._issue_rs(link, slot, bidx, ev)
+        runs: dict[int, tuple[int, list[int]]] = {}
+        for bidx in bidxs:
+            for link, slot in self._fresh_now.pop(bidx, ()):
+                cur = runs.get(link)
+                if cur is not None and cur[0] != slot:
+                    self._issue_rs(link, cur[0], cur[1], ev)
+                    cur = None
+                if cur is None:
+                    cur = runs[link] = (slot, [])
+                cur[1].append(bidx)
+        for link, (slot, bl) in runs.items():
+            self._issue_rs(link, slot, bl, ev)
         if self.placement == "bucket":
-            for slot, k in self._due_now:
-                self._issue_update(slot, k, bidx, ev)
-        self._fired[bidx] = True
+            for bidx in bidxs:
+                for slot, k in self._due_now:
+                    self._issue_update(slot, k, bidx, ev)
+        for bidx in bidxs:
+            self._fired[bidx] = True
 
     def _run_iteration(self, it: IterPlan, batch, loss_fn: Callable) -> torch.Tensor:
         """Issue one iteration's device work on the current stream (+ link and
@@ -640,8 +676,7 @@ class DeftDataParallel:
             self._updates_at_start(comp, it.due)
         ev_fwd = torch.cuda.Event()
         ev_fwd.record(comp)
-        for link, slot, bidx in it.fwd:
-            self._issue_rs(link, slot, bidx, ev_fwd)
+        self._issue_planned(it.fwd, ev_fwd)
         with self._autocast():
             loss = loss_fn(self.module, batch)
         if self.placement == "start":
@@ -663,8 +698,7 @@ class DeftDataParallel:
             self._gather_slot = None
         ev_bwd = torch.cuda.Event()
         ev_bwd.record(comp)
-        for link, slot, bidx in it.bwd:
-            self._issue_rs(link, slot, bidx, ev_bwd)
+        self._issue_planned(it.bwd, ev_bwd)
         self._fresh_now = dict(it.fresh)
         self._due_now = it.due if self.placement != "start" else ()
         self._pending = list(self._bucket_nparams)
@@ -674,9 +708,9 @@ class DeftDataParallel:
             loss.backward()
         finally:
             self._in_step = False
-        for b in range(len(self.buckets)):      # buckets whose params got no gradient
-            if not self._fired[b]:
-                self._bucket_ready(b)
+        unfired = [b for b in range(len(self.buckets)) if not self._fired[b]]
+        if unfired:                             # buckets whose params got no gradient
+            self._buckets_ready(unfired)
         if self._gather_slot is not None:
             # every gather done before the slot is read by an update on this
             # stream and before autograd's gradient buffers can be reused
