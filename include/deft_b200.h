@@ -204,10 +204,13 @@ deft_status_t deft_sgd_momentum_update_multi(const void* d_grad, int32_t grad_dt
  * land in their bucket's contiguous slot range in one launch (the store half
  * of scheduler.py:223-233's store-or-merge; merges accumulate in place).
  * d_srcs / dst_offsets / byte_lens are HOST arrays (copied into the kernel
- * parameters, so CUDA-graph captures keep them). */
+ * parameters, so CUDA-graph captures keep them).  Ranges of at least
+ * ce_min_bytes go through the copy engines instead (no SMs: for a gather that
+ * runs beside the backward); 0 = kernel only, < 0 = DEFT_GATHER_CE_MIN
+ * (default 4 MiB). */
 deft_status_t deft_gather_segments(void* d_dst, const void* const* d_srcs,
                                    const int64_t* dst_offsets, const int64_t* byte_lens,
-                                   int32_t count, void* stream);
+                                   int32_t count, int64_t ce_min_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -82,7 +82,8 @@ def _declare(lib):
                                              c_f32, c_f32, c_vp, c_vp]),
         "deft_sgd_momentum_update": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_i64, c_f32,
                                              c_f32, c_f32, c_vp]),
-        "deft_gather_segments": (c_i32, [c_vp, P(c_vp), P(c_i64), P(c_i64), c_i32, c_vp]),
+        "deft_gather_segments": (c_i32, [c_vp, P(c_vp), P(c_i64), P(c_i64), c_i32, c_i64,
+                                         c_vp]),
         "deft_sgd_momentum_update_multi": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_i32,
                                                    P(c_i64), P(c_i64), P(c_f32), c_f32, c_f32,
                                                    c_vp]),

@@ -140,14 +140,16 @@ class BucketComm:
                                                c_vp(stream.cuda_stream)),
               "deft_bucket_update")
 
-    def gather(self, slot: int, srcs, byte_offsets, byte_lens, stream) -> None:
-        """Gather device byte ranges into slot `slot` (deft_gather_segments)."""
+    def gather(self, slot: int, srcs, byte_offsets, byte_lens, stream,
+               ce_min_bytes: int = 0) -> None:
+        """Gather device byte ranges into slot `slot` (deft_gather_segments);
+        ranges >= ce_min_bytes (> 0) are copied by the copy engines."""
         n = len(srcs)
         esz = 2 if self.grad_dtype == torch.bfloat16 else 4
         dst = self._g.ptr.value + slot * self.slot_elems * esz
         check(_native.lib().deft_gather_segments(
             c_vp(dst), (c_vp * n)(*srcs), (ctypes.c_int64 * n)(*byte_offsets),
-            (ctypes.c_int64 * n)(*byte_lens), n, c_vp(stream.cuda_stream)),
+            (ctypes.c_int64 * n)(*byte_lens), n, int(ce_min_bytes), c_vp(stream.cuda_stream)),
             "deft_gather_segments")
 
     def update_multi(self, slot: int, ranges, scale: float, lr: float, momentum: float,

@@ -628,9 +628,10 @@ __global__ void __launch_bounds__(kLocalThreads) gather_kernel(char* __restrict_
 }  // namespace deft
 
 namespace deft {
-// Segments of at least this many bytes are copied by the copy engines
-// (cudaMemcpyAsync D2D: no SMs, so the concurrent backward keeps all of them);
-// the rest by gather_kernel.  DEFT_GATHER_CE_MIN (bytes; 0 = kernel only).
+// Default copy-engine threshold of launch_gather (ce_min < 0): segments of at
+// least this many bytes are copied by the copy engines (cudaMemcpyAsync D2D: no
+// SMs, so a concurrent backward keeps all of them); the rest by gather_kernel.
+// DEFT_GATHER_CE_MIN (bytes; 0 = kernel only).
 static int64_t gather_ce_min() {
   static int64_t v = [] {
     const char* e = getenv("DEFT_GATHER_CE_MIN");
@@ -640,8 +641,9 @@ static int64_t gather_ce_min() {
 }
 
 cudaError_t launch_gather(char* dst, const void* const* srcs, const int64_t* dst_off,
-                          const int64_t* lens, int32_t count, cudaStream_t stream) {
-  const int64_t ce_min = gather_ce_min();
+                          const int64_t* lens, int32_t count, int64_t ce_min,
+                          cudaStream_t stream) {
+  if (ce_min < 0) ce_min = gather_ce_min();
   std::vector<int32_t> small;
   small.reserve(count);
   for (int32_t k = 0; k < count; ++k) {
@@ -1031,9 +1033,13 @@ bool launch_reduce_scatter_tma_multi(const PeerPtrs& P, int rank, int world, int
   const int align = dtype == 0 ? 4 : 8;
   for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
     ChunkTable t{};
-    const int64_t owned = build_chunk_table(t, s0, count, offsets, numels, rank, world, align,
-                                            rs_chunk_for(world, dtype));
-    int grid = (int)((owned + 32767) / 32768);
+    build_chunk_table(t, s0, count, offsets, numels, rank, world, align,
+                      rs_chunk_for(world, dtype));
+    // the grid must be the same on every rank (block b meets block b of each
+    // peer): a function of the bucket sizes only, not of this rank's shards
+    int64_t per = 0;
+    for (int k = 0; k < t.count; ++k) per += (numels[s0 + k] + world - 1) / world;
+    int grid = (int)((per + 32767) / 32768);
     if (grid < 1) grid = 1;
     if (grid > rs_tma_blocks()) grid = rs_tma_blocks();
     if (dtype == 0)

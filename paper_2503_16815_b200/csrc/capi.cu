@@ -548,12 +548,12 @@ extern "C" deft_status_t deft_sgd_momentum_update_multi(const void* d_grad, int3
 extern "C" deft_status_t deft_gather_segments(void* d_dst, const void* const* d_srcs,
                                               const int64_t* dst_offsets,
                                               const int64_t* byte_lens, int32_t count,
-                                              void* stream) {
+                                              int64_t ce_min_bytes, void* stream) {
   if (count <= 0) return DEFT_OK;
   if (!d_dst || !d_srcs || !dst_offsets || !byte_lens)
     return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_gather_segments: null argument");
   cudaError_t e = launch_gather(reinterpret_cast<char*>(d_dst), d_srcs, dst_offsets, byte_lens,
-                                count, (cudaStream_t)stream);
+                                count, ce_min_bytes, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "gather_kernel");
   return DEFT_OK;
 }

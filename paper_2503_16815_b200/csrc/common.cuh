@@ -124,6 +124,7 @@ int64_t sched_smem_bytes(int64_t words);
 cudaError_t launch_scheduler(const SchedArgs& a, int32_t instances, int64_t smem,
                              cudaStream_t stream);
 cudaError_t launch_gather(char* dst, const void* const* srcs, const int64_t* dst_off,
-                          const int64_t* lens, int32_t count, cudaStream_t stream);
+                          const int64_t* lens, int32_t count, int64_t ce_min,
+                          cudaStream_t stream);
 
 }  // namespace deft

@@ -630,12 +630,17 @@ class DeftDataParallel:
                 lens.append((hi - lo) * esz)
         if srcs:
             stream = torch.cuda.current_stream(self.device)
-            self.comm.gather(slot, srcs, offs, lens, stream)
+            # beside the backward (W > 1) large ranges use the copy engines
+            self.comm.gather(slot, srcs, offs, lens, stream,
+                             ce_min_bytes=-1 if self.world > 1 else 0)
 
     def _buckets_ready(self, bidxs: list[int]):
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))
-        if self._gather_slot is not None:
+        if self._gather_slot is not None and self.world == 1:
+            # one GPU: nothing waits for the slot before the update -- copy in line
+            self._gather_buckets(bidxs, self._gather_slot)
+        elif self._gather_slot is not None:
             # copy the fresh gradients into the slot on the gather stream: the
             # backward continues while they move (the compute stream joins it
             # once, after the whole backward); the buckets' transfers wait for it
@@ -711,7 +716,7 @@ class DeftDataParallel:
         unfired = [b for b in range(len(self.buckets)) if not self._fired[b]]
         if unfired:                             # buckets whose params got no gradient
             self._buckets_ready(unfired)
-        if self._gather_slot is not None:
+        if self._gather_slot is not None and self.world > 1:
             # every gather done before the slot is read by an update on this
             # stream and before autograd's gradient buffers can be reused
             comp.wait_stream(self.gather_stream)
