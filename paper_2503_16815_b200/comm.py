@@ -69,13 +69,20 @@ class BucketComm:
         self.device = device
         esz = 2 if grad_dtype == torch.bfloat16 else 4
         ipc = world > 1
-        self.grads, self._g = region_tensor(n_slots * slot_elems * esz, grad_dtype, ipc, device)
-        self.grads = self.grads.view(n_slots, slot_elems)
+        # slots start 256-byte aligned (the kernels' vector and TMA bulk accesses
+        # are aligned relative to the slot base)
+        self.slot_stride = -(-slot_elems // 128) * 128
+        self.grads, self._g = region_tensor(n_slots * self.slot_stride * esz, grad_dtype, ipc,
+                                            device)
+        self.grads = self.grads.view(n_slots, self.slot_stride)[:, :slot_elems]
         # parameters share the gradient dtype (autograd requires it); bf16 models
         # keep an fp32 master copy that only the update kernel touches
-        self.params, self._p = region_tensor(slot_elems * esz, grad_dtype, ipc, device)
-        self.master = (torch.empty(slot_elems, dtype=torch.float32, device=device)
-                       if grad_dtype == torch.bfloat16 else None)
+        # padded like a slot, so every range the C-ABI accepts is inside all buffers
+        self.params, self._p = region_tensor(self.slot_stride * esz, grad_dtype, ipc, device)
+        self.params = self.params[:slot_elems]
+        self._master_buf = (torch.zeros(self.slot_stride, dtype=torch.float32, device=device)
+                            if grad_dtype == torch.bfloat16 else None)
+        self.master = self._master_buf[:slot_elems] if self._master_buf is not None else None
         fbytes = int(_native.lib().deft_comm_flag_bytes(world))
         self.flags, self._f = region_tensor(fbytes, torch.uint8, ipc, device)
         self._opened: list[c_vp] = []
@@ -87,7 +94,8 @@ class BucketComm:
         h = c_vp()
         check(_native.lib().deft_comm_create(
             rank, world, arr(maps.grads), arr(maps.params), arr(maps.flags),
-            c_vp(self.master.data_ptr() if self.master is not None else None), slot_elems, n_slots,
+            c_vp(self.master.data_ptr() if self.master is not None else None), self.slot_stride,
+            n_slots,
             DTYPE_BF16 if grad_dtype == torch.bfloat16 else DTYPE_F32, ctypes.byref(h)),
             "deft_comm_create")
         self._h = h
@@ -146,7 +154,7 @@ class BucketComm:
         ranges >= ce_min_bytes (> 0) are copied by the copy engines."""
         n = len(srcs)
         esz = 2 if self.grad_dtype == torch.bfloat16 else 4
-        dst = self._g.ptr.value + slot * self.slot_elems * esz
+        dst = self._g.ptr.value + slot * self.slot_stride * esz
         check(_native.lib().deft_gather_segments(
             c_vp(dst), (c_vp * n)(*srcs), (ctypes.c_int64 * n)(*byte_offsets),
             (ctypes.c_int64 * n)(*byte_lens), n, int(ce_min_bytes), c_vp(stream.cuda_stream)),

@@ -86,6 +86,7 @@ class DeftConfig:
     # input layer first).  Synchronous: updates of iteration t visible from t+1.
     scheme: str = "deft"
     graph_warmup: int = 1                   # eager runs of a shape before it is captured
+    defer_tail: bool = True                 # delayed schedules: last transfers -> next iteration
 
 
 class _Bucket:
@@ -378,8 +379,8 @@ class DeftDataParallel:
         else:
             self.scheduler = DeftScheduler(part, cluster, mult)
         self.capacity_multiplier = mult
-        blocks = self.cfg.update_blocks or (32 if self.placement == "start" else 0)
-        self.comm.set_update_blocks(blocks)
+        self._update_blocks = self.cfg.update_blocks or (32 if self.placement == "start" else 0)
+        self.comm.set_update_blocks(self._update_blocks)
         # delayed (DeFT): visible from t+2; synchronous baselines: from t+1
         lag = (1 if self.placement == "start" else 0) if self.sync else \
             (2 if self.placement == "start" else 1)
@@ -409,6 +410,11 @@ class DeftDataParallel:
         self._fwd_wait = {}
         if self.placement == "start":
             self._install_forward_waits()
+        # delayed schedules at W > 1 with per-iteration joins: the backward's last
+        # fresh transfers start with the next iteration (see _buckets_ready)
+        self._deferred: list[tuple[int, int, tuple]] = []
+        self._defer_tail = (not self.sync and self.world > 1 and self._sequential
+                            and self.cfg.defer_tail)
         return part
 
     def decisions(self, t: int) -> tuple[ScheduleDecision, ScheduleDecision]:
@@ -444,7 +450,8 @@ class DeftDataParallel:
         b.record(stream)
         self._events_t.append((kind, a, b, nbytes))
 
-    def _issue_rs(self, link: int, slot: int, bidxs: list[int], release: torch.cuda.Event):
+    def _issue_rs(self, link: int, slot: int, bidxs: list[int], release: torch.cuda.Event,
+                  track: bool = False):
         """The buckets one release point puts on one link, in plan order: ONE
         reduce-scatter launch (one cross-rank barrier) on the link's stream."""
         if self.world == 1 or not bidxs:
@@ -459,9 +466,10 @@ class DeftDataParallel:
         self._timed("reduce_scatter", s,
                     lambda: self.comm.reduce_scatter_multi(self.channel_of_link[link], slot,
                                                            ranges, s), nbytes)
-        if not self._sequential or self.planner.lag == 0:
+        if track or not self._sequential or self.planner.lag == 0:
             # an update waits for it: always when streams run ahead (eager, async),
-            # and within the iteration for synchronous schedules (lag 0)
+            # within the iteration for synchronous schedules (lag 0), and for
+            # transfers deferred into the next iteration
             ev = torch.cuda.Event()
             ev.record(s)
             for b in bidxs:
@@ -557,7 +565,10 @@ class DeftDataParallel:
         self._touched[id(s)] = s
         self._fwd_wait = {}
         esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
-        for group in self._start_groups():
+        for gi, group in enumerate(self._start_groups()):
+            # the forward waits for the first group with the GPU otherwise idle:
+            # full grid; later groups overlap the forward on the small budget
+            self.comm.set_update_blocks(0 if gi == 0 else self._update_blocks)
             ranges = [(self.buckets[b].lo, self.buckets[b].hi) for b in group]
             elems = sum(hi - lo for lo, hi in ranges)
             nbytes = elems * 20 if self.world == 1 else elems * esz * (self.world - 1) // self.world
@@ -574,6 +585,7 @@ class DeftDataParallel:
             ev.record(s)
             for b in group:
                 self._fwd_wait[b] = ev
+        self.comm.set_update_blocks(self._update_blocks)
 
     def _updates_at_end(self, comp):
         """All due updates after the whole backward (every no-read window is open):
@@ -651,24 +663,36 @@ class DeftDataParallel:
                 self._gather_buckets(bidxs, self._gather_slot)
             ev = torch.cuda.Event()
             ev.record(gs)
+        # the backward's last release: with delayed updates its transfers may
+        # start with the next iteration instead (they are needed an iteration
+        # later), so the per-iteration join does not wait for them
+        last = self._defer_tail and sum(self._fired) + len(bidxs) == len(self.buckets)
+        issue = (lambda link, slot, bl: self._deferred.append((link, slot, tuple(bl)))) \
+            if last else (lambda link, slot, bl: self._issue_rs(link, slot, bl, ev))
         runs: dict[int, tuple[int, list[int]]] = {}
         for bidx in bidxs:
             for link, slot in self._fresh_now.pop(bidx, ()):
                 cur = runs.get(link)
                 if cur is not None and cur[0] != slot:
-                    self._issue_rs(link, cur[0], cur[1], ev)
+                    issue(link, cur[0], cur[1])
                     cur = None
                 if cur is None:
                     cur = runs[link] = (slot, [])
                 cur[1].append(bidx)
         for link, (slot, bl) in runs.items():
-            self._issue_rs(link, slot, bl, ev)
+            issue(link, slot, bl)
         if self.placement == "bucket":
             for bidx in bidxs:
                 for slot, k in self._due_now:
                     self._issue_update(slot, k, bidx, ev)
         for bidx in bidxs:
             self._fired[bidx] = True
+
+    def _issue_deferred(self, release: torch.cuda.Event):
+        """Transfers the previous iteration deferred from its backward's end."""
+        deferred, self._deferred = self._deferred, []
+        for link, slot, bl in deferred:
+            self._issue_rs(link, slot, list(bl), release, track=True)
 
     def _run_iteration(self, it: IterPlan, batch, loss_fn: Callable) -> torch.Tensor:
         """Issue one iteration's device work on the current stream (+ link and
@@ -677,10 +701,11 @@ class DeftDataParallel:
         self._touched = {}      # side streams forked from `comp` in this iteration
         if not self._sequential and self._version_ready is not None:
             comp.wait_event(self._version_ready)   # theta^(t) complete
-        if self.placement == "start" and it.due:
-            self._updates_at_start(comp, it.due)
         ev_fwd = torch.cuda.Event()
         ev_fwd.record(comp)
+        self._issue_deferred(ev_fwd)
+        if self.placement == "start" and it.due:
+            self._updates_at_start(comp, it.due)
         self._issue_planned(it.fwd, ev_fwd)
         with self._autocast():
             loss = loss_fn(self.module, batch)
@@ -728,6 +753,9 @@ class DeftDataParallel:
         if self._sequential:
             for s in self._touched.values():   # join (only streams forked this iteration)
                 comp.wait_stream(s)
+            # everything issued so far is complete once the join is: no event may
+            # carry over (inside a CUDA-graph capture it could not be waited on)
+            self._rs_done.clear()
         else:
             ev = torch.cuda.Event()
             ev.record(self.update_stream)
@@ -835,15 +863,17 @@ class DeftDataParallel:
                 batch = self._static_inputs(batch)
             return self._run_iteration(it, batch, loss_fn)
         static = self._static_inputs(batch)
-        hit = self._graphs.get(it.key)
+        key = (it.key, tuple(self._deferred))   # deferred transfers run in this graph
+        hit = self._graphs.get(key)
         if hit is not None:
-            g, loss, n = hit
+            g, loss, n, deferred = hit
+            self._deferred = list(deferred)
             g.replay()
             self._replayed_native += n
             self.last_step_kind = "replay"
             return loss
-        seen = self._seen.get(it.key, 0)
-        self._seen[it.key] = seen + 1
+        seen = self._seen.get(key, 0)
+        self._seen[key] = seen + 1
         if seen < self.cfg.graph_warmup or self._freeze_graphs:
             self.last_step_kind = "eager"
             return self._run_iteration(it, static, loss_fn)
@@ -854,7 +884,7 @@ class DeftDataParallel:
             loss = self._run_iteration(it, static, loss_fn)
         n = _native.launch_count() - n0
         self._captured_native += n
-        self._graphs[it.key] = (g, loss, n)
+        self._graphs[key] = (g, loss, n, tuple(self._deferred))
         g.replay()
         self._replayed_native += n
         self.last_step_kind = "capture"
@@ -866,6 +896,17 @@ class DeftDataParallel:
         applied here (they would otherwise run at the start of iteration t); groups
         still in flight stay unapplied, as in the reference where unaccounted
         iterations are still in flight."""
+        if getattr(self, "_deferred", None):
+            caller = torch.cuda.current_stream(self.device)
+            self.compute_stream.wait_stream(caller)
+            with torch.cuda.stream(self.compute_stream):
+                self._touched = {}
+                ev = torch.cuda.Event()
+                ev.record(self.compute_stream)
+                self._issue_deferred(ev)
+                for st in self._touched.values():
+                    self.compute_stream.wait_stream(st)
+            caller.wait_stream(self.compute_stream)
         if self.placement == "start" and hasattr(self, "planner"):
             due, freed = self.planner.take_pending()
             self.updates_applied += len(due)
