@@ -650,8 +650,10 @@ class DeftDataParallel:
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))
         if self._gather_slot is not None and self.world == 1:
-            # one GPU: nothing waits for the slot before the update -- copy in line
+            # one GPU: no transfer follows -- copy in line on the compute stream
             self._gather_buckets(bidxs, self._gather_slot)
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(self.device))
         elif self._gather_slot is not None:
             # copy the fresh gradients into the slot on the gather stream: the
             # backward continues while they move (the compute stream joins it
