@@ -363,10 +363,12 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
         if ddp.placement == "end":
             ddp.comm.update_multi(slot, [(b.lo, b.hi) for b in ddp.buckets], 1.0, 0.0, 0.9,
                                   ddp.mom, s)
-        elif ddp.placement == "start":
-            for g in ddp._start_groups():
+        elif ddp.placement == "start":   # first group on the full grid, as in the step
+            for gi, g in enumerate(ddp._start_groups()):
+                ddp.comm.set_update_blocks(0 if gi == 0 else ddp._update_blocks)
                 ddp.comm.update_multi(slot, [(ddp.buckets[b].lo, ddp.buckets[b].hi) for b in g],
                                       1.0, 0.0, 0.9, ddp.mom, s)
+            ddp.comm.set_update_blocks(ddp._update_blocks)
         else:
             for b in ddp.buckets:
                 ddp.comm.update(slot, b.lo, b.hi - b.lo, 0.0, 0.9, 1.0, ddp.mom, s)
@@ -625,13 +627,15 @@ def main():
         avg_ms = r["ms"] / r["launches"]
         in_step = (r["bytes"] / r["launches"]) / (avg_ms / 1e3) / 1e9
     achieved = iso[kind]["achieved_gbs"]
+    # the kernels the step launches (csrc/bucket_comm.cu; env overrides as there)
+    tma_upd = os.environ.get("DEFT_UPDATE_IMPL", "tma")[:1] != "l"
+    tma_rs = os.environ.get("DEFT_RS_IMPL", "tma")[:1] != "l"
     upd_name = "sgd_local_kernel" if world == 1 else (
-        "update_allgather_multi_kernel" if ddp.placement in ("end", "start")
-        else "update_allgather_kernel")
-    traffic = ncu_traffic(upd_name if kind == "update" else "reduce_scatter_kernel",
-                          args.model, world)
-    roof = {"kernel": {"update": upd_name,
-                       "reduce_scatter": "reduce_scatter_kernel"}[kind],
+        ("update_allgather_tma_kernel" if tma_upd else "update_allgather_multi_kernel")
+        if ddp.placement in ("end", "start") else "update_allgather_kernel")
+    rs_name = "reduce_scatter_tma_kernel" if tma_rs else "reduce_scatter_kernel"
+    traffic = ncu_traffic(upd_name if kind == "update" else rs_name, args.model, world)
+    roof = {"kernel": {"update": upd_name, "reduce_scatter": rs_name}[kind],
             "bound": "hbm" if hbm_bound else "nvlink",
             "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
