@@ -353,6 +353,21 @@ extern "C" deft_status_t deft_comm_create(int32_t rank, int32_t world, void* con
       return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_comm_create: flags required for world > 1");
     }
   }
+  if (world > 1) {
+    // copy-engine staging sized up front for any transfer list over one slot (the
+    // (W-1) peer shards of every bucket + 16-byte stride padding for up to 4096
+    // buckets): growing it later would synchronise, which a CUDA-graph capture
+    // cannot do
+    const size_t esz = grad_dtype == DEFT_DTYPE_F32 ? 4 : 2;
+    const size_t need = (size_t)(world - 1) *
+                        ((size_t)(slot_elems + world - 1) / world + (size_t)24 * 4096) * esz;
+    cudaError_t e = cudaMalloc(&c->staging, need);
+    if (e != cudaSuccess) {
+      delete c;
+      return cuda_fail(e, "deft_comm_create: staging");
+    }
+    c->staging_bytes = need;
+  }
   *out = c;
   return DEFT_OK;
 }

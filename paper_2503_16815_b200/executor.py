@@ -85,7 +85,7 @@ class DeftConfig:
     # backward end, measured buckets) / "priority" (partition_by_size blocks,
     # input layer first).  Synchronous: updates of iteration t visible from t+1.
     scheme: str = "deft"
-    graph_warmup: int = 1                   # eager runs of a shape before it is captured
+    graph_warmup: int = 2                   # eager iterations before any capture
     defer_tail: bool = True                 # delayed schedules: last transfers -> next iteration
 
 
@@ -399,7 +399,7 @@ class DeftDataParallel:
         self._freeze_graphs = False
         self.graph_choice = None
         self._graphs: dict = {}
-        self._seen: dict = {}
+        self._eager_runs = 0
         self._static = None
         self._pool = torch.cuda.graph_pool_handle() if self._use_graphs else None
         self._captured_native = 0
@@ -806,7 +806,7 @@ class DeftDataParallel:
         caller.wait_stream(self.compute_stream)
         return loss
 
-    def warm_up(self, batch, loss_fn: Callable, min_steps: int = 3, max_steps: int = 64,
+    def warm_up(self, batch, loss_fn: Callable, min_steps: int = 3, max_steps: int = 96,
                 steady: int = 6, compare: int = 4) -> int:
         """Run steps until the last `steady` were all graph replays (every
         steady-state iteration shape captured).  Then, with ``cuda_graphs="auto"``,
@@ -850,7 +850,6 @@ class DeftDataParallel:
         import gc
         torch.cuda.synchronize(self.device)
         self._graphs.clear()
-        self._seen.clear()
         gc.collect()
         torch.cuda.empty_cache()
 
@@ -888,9 +887,12 @@ class DeftDataParallel:
             self._replayed_native += n
             self.last_step_kind = "replay"
             return loss
-        seen = self._seen.get(key, 0)
-        self._seen[key] = seen + 1
-        if seen < self.cfg.graph_warmup or self._freeze_graphs:
+        # a new shape is captured on first sight once the process itself is warm
+        # (allocator, library handles, autotuning: `graph_warmup` eager
+        # iterations of any shape) -- the model's compute is the same in every
+        # shape, only the communication plan differs
+        if self._eager_runs < self.cfg.graph_warmup or self._freeze_graphs:
+            self._eager_runs += 1
             self.last_step_kind = "eager"
             return self._run_iteration(it, static, loss_fn)
         self.compute_stream.synchronize()
