@@ -62,7 +62,7 @@ def parse():
                     help="scale the measured comm times before planning (slower-link / "
                          "update-frequency sweep: >1 makes DeFT merge iterations)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--h2d-chunks", type=int, default=1,
+    ap.add_argument("--h2d-chunks", type=int, default=32,
                     help="e2e: split each step's host->device input copy into this many "
                          "batch slices")
     return ap.parse_args()

@@ -829,7 +829,9 @@ class DeftDataParallel:
             self._release_graphs()
             self.graph_choice = {"use_graphs": False, "reason": "no steady-state shape",
                                  "graphs_released": True}
-            return n
+            for _ in range(min_steps):        # the allocator re-grows eagerly
+                self.train_step(batch, loss_fn)
+            return n + min_steps
         # from now on unseen iteration shapes run eagerly instead of being captured
         self._freeze_graphs = True
         if self.cfg.cuda_graphs == "auto" and self._use_graphs and compare > 0:
