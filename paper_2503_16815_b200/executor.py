@@ -845,6 +845,9 @@ class DeftDataParallel:
                                  "use_graphs": self._use_graphs}
             if not self._use_graphs:
                 self._release_graphs()
+                for _ in range(2):            # the allocator re-grows eagerly
+                    self.train_step(batch, loss_fn)
+                n += 2
             n += 2 * compare + 2
         return n
 
