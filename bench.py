@@ -372,9 +372,9 @@ def isolated_kernels(ddp, world, dist, device, reps=10):
                 ddp.comm.update_multi(slot, [(ddp.buckets[b].lo, ddp.buckets[b].hi) for b in g],
                                       1.0, 0.0, 0.9, ddp.mom, s)
             ddp.comm.set_update_blocks(ddp._update_blocks)
-        else:
+        else:                             # "bucket": one launch per bucket
             for b in ddp.buckets:
-                ddp.comm.update(slot, b.lo, b.hi - b.lo, 0.0, 0.9, 1.0, ddp.mom, s)
+                ddp.comm.update_multi(slot, [(b.lo, b.hi)], 1.0, 0.0, 0.9, ddp.mom, s)
     with torch.cuda.stream(s):
         run("update", updates, upd_bytes)
         if world > 1:
@@ -641,7 +641,7 @@ def main():
     tma_rs = os.environ.get("DEFT_RS_IMPL", "tma")[:1] != "l"
     upd_name = "sgd_local_kernel" if world == 1 else (
         ("update_allgather_tma_kernel" if tma_upd else "update_allgather_multi_kernel")
-        if ddp.placement in ("end", "start") else "update_allgather_kernel")
+        if ddp.placement in ("end", "start", "bucket") else "update_allgather_kernel")
     rs_name = "reduce_scatter_tma_kernel" if tma_rs else "reduce_scatter_kernel"
     traffic = ncu_traffic(upd_name if kind == "update" else rs_name, args.model, world)
     roof = {"kernel": {"update": upd_name, "reduce_scatter": rs_name}[kind],

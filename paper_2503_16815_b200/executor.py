@@ -379,7 +379,8 @@ class DeftDataParallel:
         else:
             self.scheduler = DeftScheduler(part, cluster, mult)
         self.capacity_multiplier = mult
-        self._update_blocks = self.cfg.update_blocks or (32 if self.placement == "start" else 0)
+        self._update_blocks = self.cfg.update_blocks or (
+            32 if self.placement in ("start", "bucket") else 0)
         self.comm.set_update_blocks(self._update_blocks)
         # delayed (DeFT): visible from t+2; synchronous baselines: from t+1
         lag = (1 if self.placement == "start" else 0) if self.sync else \
@@ -490,23 +491,25 @@ class DeftDataParallel:
         for link, (slot, bl) in runs.items():
             self._issue_rs(link, slot, bl, release)
 
-    def _issue_update(self, slot: int, k: int, bidx: int, window_open: torch.cuda.Event):
-        b = self.buckets[bidx]
+    def _issue_updates(self, bidxs: list[int], window_open: torch.cuda.Event):
+        """"bucket" placement: the due updates of the buckets whose backward just
+        ended, one multi-segment launch per update event on the update stream
+        (small CTA budget: it runs beside the rest of the backward)."""
         s = self.update_stream
         s.wait_event(window_open)
         self._touched[id(s)] = s
-        rs = self._rs_done.pop((slot, bidx), None)
-        if rs is not None:
-            s.wait_event(rs)
+        ranges = [(self.buckets[b].lo, self.buckets[b].hi) for b in bidxs]
+        elems = sum(hi - lo for lo, hi in ranges)
         esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
-        if self.world == 1:   # HBM: read g, v, p; write v, p
-            nbytes = (b.hi - b.lo) * 20
-        else:                 # NVLink: the owned shard's new params stored to W-1 peers
-            nbytes = (b.hi - b.lo) * esz * (self.world - 1) // self.world
-        self._timed("update", s,
-                    lambda: self.comm.update(slot, b.lo, b.hi - b.lo, self.cfg.lr,
-                                             self.cfg.momentum, 1.0 / (self.world * k),
-                                             self.mom, s), nbytes)
+        nbytes = elems * 20 if self.world == 1 else elems * esz * (self.world - 1) // self.world
+        for slot, k in self._due_now:
+            for b in bidxs:
+                rs = self._rs_done.pop((slot, b), None)
+                if rs is not None:
+                    s.wait_event(rs)
+            self._timed("update", s, lambda: self.comm.update_multi(
+                slot, ranges, 1.0 / (self.world * k), self.cfg.lr, self.cfg.momentum,
+                self.mom, s), nbytes)
 
     def _install_forward_waits(self):
         """"start" placement: the forward pre-hook of every module that owns
@@ -683,10 +686,8 @@ class DeftDataParallel:
                 cur[1].append(bidx)
         for link, (slot, bl) in runs.items():
             issue(link, slot, bl)
-        if self.placement == "bucket":
-            for bidx in bidxs:
-                for slot, k in self._due_now:
-                    self._issue_update(slot, k, bidx, ev)
+        if self.placement == "bucket" and self._due_now:
+            self._issue_updates(bidxs, ev)
         for bidx in bidxs:
             self._fired[bidx] = True
 
