@@ -44,7 +44,7 @@ from .errors import DeftError, InternalInvariantError
 from .partition import PartitionConfig, element_ranges, partition_buckets, partition_by_size
 from .preserver import WalkParams, feedback_loop
 from .profiles import BucketProfile, ClusterSpec, LinkSpec, ModelProfile
-from .planner import ExecutionPlanner, IterPlan
+from .planner import ExecutionPlanner, IterPlan, release_runs, start_groups
 from .scheduler import (DeftScheduler, OrderScheduler, ScheduleDecision, priority_order,
                         wfbp_order)
 
@@ -479,16 +479,7 @@ class DeftDataParallel:
     def _issue_planned(self, transfers, release: torch.cuda.Event):
         """Stage-plan transfers (link, slot, bucket) released together: per link,
         consecutive same-slot runs in plan order become one launch each."""
-        runs: dict[int, tuple[int, list[int]]] = {}
-        for link, slot, bidx in transfers:
-            cur = runs.get(link)
-            if cur is not None and cur[0] != slot:
-                self._issue_rs(link, cur[0], cur[1], release)
-                cur = None
-            if cur is None:
-                cur = runs[link] = (slot, [])
-            cur[1].append(bidx)
-        for link, (slot, bl) in runs.items():
+        for link, slot, bl in release_runs(transfers):
             self._issue_rs(link, slot, bl, release)
 
     def _issue_updates(self, bidxs: list[int], window_open: torch.cuda.Event):
@@ -536,25 +527,9 @@ class DeftDataParallel:
                 self._hooks.append(m.register_forward_pre_hook(pre))
 
     def _start_groups(self) -> list[list[int]]:
-        """Consecutive buckets in forward order (input side first) coalesced into at
-        most `start_groups` update launches: a small first group (the forward's
-        first modules wait only for it), then groups of similar size.  One update
-        launch per group."""
         if getattr(self, "_groups_cache", None) is None:
-            order = list(range(len(self.buckets) - 1, -1, -1))
-            n_groups = max(1, min(self.cfg.start_groups, len(order)))
-            first = self.total / (4 * n_groups)
-            step = (self.total - first) / max(1, n_groups - 1)
-            groups, cur, acc = [], [], 0
-            for b in order:
-                cur.append(b)
-                acc += self.buckets[b].hi - self.buckets[b].lo
-                if acc >= first + step * len(groups) and len(groups) < n_groups - 1:
-                    groups.append(cur)
-                    cur = []
-            if cur:
-                groups.append(cur)
-            self._groups_cache = groups
+            self._groups_cache = start_groups([b.hi - b.lo for b in self.buckets],
+                                              self.cfg.start_groups)
         return self._groups_cache
 
     def _updates_at_start(self, comp, due):
@@ -674,17 +649,9 @@ class DeftDataParallel:
         last = self._defer_tail and sum(self._fired) + len(bidxs) == len(self.buckets)
         issue = (lambda link, slot, bl: self._deferred.append((link, slot, tuple(bl)))) \
             if last else (lambda link, slot, bl: self._issue_rs(link, slot, bl, ev))
-        runs: dict[int, tuple[int, list[int]]] = {}
-        for bidx in bidxs:
-            for link, slot in self._fresh_now.pop(bidx, ()):
-                cur = runs.get(link)
-                if cur is not None and cur[0] != slot:
-                    issue(link, cur[0], cur[1])
-                    cur = None
-                if cur is None:
-                    cur = runs[link] = (slot, [])
-                cur[1].append(bidx)
-        for link, (slot, bl) in runs.items():
+        fresh = [(link, slot, bidx) for bidx in bidxs
+                 for link, slot in self._fresh_now.pop(bidx, ())]
+        for link, slot, bl in release_runs(fresh):
             issue(link, slot, bl)
         if self.placement == "bucket" and self._due_now:
             self._issue_updates(bidxs, ev)

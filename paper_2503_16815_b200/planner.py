@@ -129,3 +129,51 @@ class ExecutionPlanner:
         fresh_t = tuple(sorted((b, tuple(v)) for b, v in fresh.items()))
         key = (fwd, slot, new, tuple(bwd), fresh_t, due)
         return IterPlan(t, slot, new, fwd, tuple(bwd), fresh_t, due, tuple(freed), key)
+
+
+def start_groups(bucket_sizes: list[int], max_groups: int) -> list[list[int]]:
+    """"start" placement: buckets in forward order (input side = last index
+    first) coalesced into at most `max_groups` consecutive update launches -- a
+    small first group (~1/(4*max_groups) of the parameters: the forward's first
+    modules wait for it), then groups of similar size.  Returns bucket indices."""
+    order = list(range(len(bucket_sizes) - 1, -1, -1))
+    n_groups = max(1, min(max_groups, len(order)))
+    total = sum(bucket_sizes)
+    first = total / (4 * n_groups)
+    step = (total - first) / max(1, n_groups - 1)
+    groups, cur, acc = [], [], 0
+    for b in order:
+        size = bucket_sizes[b]
+        target = first + step * len(groups)
+        if (cur and len(groups) < n_groups - 1 and acc + size > target
+                and acc + size - target > target - acc):
+            # b would overshoot the target by more than it fills: the modules
+            # before it must not wait for its (large) update -- close first
+            groups.append(cur)
+            cur = []
+            target = first + step * len(groups)
+        cur.append(b)
+        acc += size
+        if acc >= target and len(groups) < n_groups - 1:
+            groups.append(cur)
+            cur = []
+    if cur:
+        groups.append(cur)
+    return groups
+
+
+def release_runs(transfers) -> list[tuple[int, int, list[int]]]:
+    """Transfers released together, as (link, slot, bucket) in plan order ->
+    one (link, slot, [buckets]) launch per consecutive same-slot run on each
+    link; per-link order is kept (a link serves its transfers in plan order,
+    simulator.py:107-129)."""
+    out: list[tuple[int, int, list[int]]] = []
+    open_run: dict[int, tuple[int, int, list[int]]] = {}
+    for link, slot, bidx in transfers:
+        cur = open_run.get(link)
+        if cur is None or cur[1] != slot:
+            cur = (link, slot, [])
+            open_run[link] = cur
+            out.append(cur)
+        cur[2].append(bidx)
+    return out

@@ -168,3 +168,34 @@ def test_two_rank_gloo_plans_agree():
     for rank, same, err in res:
         assert same, rank
         assert err < 1e-6, (rank, err)
+
+
+def test_start_groups():
+    from paper_2503_16815_b200.planner import start_groups
+    # VGG-19-like: a huge output-side bucket (fc6) and many small input-side ones
+    sizes = [4_100_000, 16_800_000, 102_800_000] + [2_400_000] * 8 + [600_000] * 4
+    g = start_groups(sizes, 8)
+    flat = [b for grp in g for b in grp]
+    assert flat == list(range(len(sizes) - 1, -1, -1))      # forward order, each once
+    assert 1 < len(g) <= 8
+    total = sum(sizes)
+    assert sum(sizes[b] for b in g[0]) <= total / 8          # small first group
+    # fc6 does not share a launch with the buckets the forward reaches before it
+    grp6 = next(grp for grp in g if 2 in grp)
+    assert all(b <= 2 for b in grp6), g
+    assert start_groups([5], 8) == [[0]]
+    assert [len(x) for x in start_groups([1] * 16, 4)] and \
+        sum(len(x) for x in start_groups([1] * 16, 4)) == 16
+    assert len(start_groups([1] * 16, 4)) <= 4
+
+
+def test_release_runs_keep_per_link_plan_order():
+    from paper_2503_16815_b200.planner import release_runs
+    tr = [(0, 3, 5), (1, 3, 4), (0, 3, 6), (0, 2, 7), (1, 3, 8), (0, 2, 9), (0, 3, 1)]
+    runs = release_runs(tr)
+    assert runs == [(0, 3, [5, 6]), (1, 3, [4, 8]), (0, 2, [7, 9]), (0, 3, [1])]
+    # per link, concatenating the runs gives back the plan order
+    for link in (0, 1):
+        assert [b for l, _, bl in runs if l == link for b in bl] == \
+            [b for l, _, b in tr if l == link]
+    assert release_runs([]) == []
