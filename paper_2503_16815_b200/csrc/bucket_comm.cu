@@ -817,7 +817,7 @@ namespace deft {
 // the concurrent backward.
 // ============================================================================
 constexpr int kTmaThreads = 256;
-constexpr int kTmaStages = 4;
+constexpr int kTmaStagesDefault = 4;   // DEFT_RS_TMA_STAGES: 4 or 6
 constexpr int kTmaStageBytes = 32 * 1024;  // W peer chunks per stage
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -900,7 +900,7 @@ __host__ __device__ constexpr int64_t rs_tma_chunk() {  // elements per peer chu
 
 // One launch reduces every segment of the table (all buckets released together
 // on this link): one entry barrier instead of one per bucket.
-template <typename T, int W>
+template <typename T, int W, int kTmaStages>
 __global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
     PeerPtrs P, int rank, int64_t slot_base, ChunkTable t) {
   using V = Vec<T>;
@@ -978,20 +978,20 @@ __global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
   }
 }
 
-template <typename T>
-static void rs_tma_dispatch(int world, int grid, cudaStream_t stream, const PeerPtrs& P,
-                            int rank, int64_t slot_base, const ChunkTable& t) {
-  const size_t smem = (size_t)kTmaStages * kTmaStageBytes;
+template <typename T, int S>
+static void rs_tma_dispatch_s(int world, int grid, cudaStream_t stream, const PeerPtrs& P,
+                              int rank, int64_t slot_base, const ChunkTable& t) {
+  const size_t smem = (size_t)S * kTmaStageBytes;
 #define DEFT_RST_CASE(WW)                                                                      \
   case WW: {                                                                                   \
     static bool attr = false;                                                                  \
     if (!attr) {                                                                               \
-      cudaFuncSetAttribute(reduce_scatter_tma_kernel<T, WW>,                                   \
+      cudaFuncSetAttribute(reduce_scatter_tma_kernel<T, WW, S>,                                \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
       attr = true;                                                                             \
     }                                                                                          \
-    reduce_scatter_tma_kernel<T, WW><<<grid, kTmaThreads, smem, stream>>>(P, rank, slot_base,  \
-                                                                          t);                  \
+    reduce_scatter_tma_kernel<T, WW, S><<<grid, kTmaThreads, smem, stream>>>(P, rank,         \
+                                                                            slot_base, t);     \
     break;                                                                                     \
   }
   switch (world) {
@@ -1000,6 +1000,23 @@ static void rs_tma_dispatch(int world, int grid, cudaStream_t stream, const Peer
     default: break;
   }
 #undef DEFT_RST_CASE
+}
+
+static int rs_tma_stages() {
+  static int v = [] {
+    const char* e = getenv("DEFT_RS_TMA_STAGES");
+    return e && atoi(e) == 6 ? 6 : kTmaStagesDefault;
+  }();
+  return v;
+}
+
+template <typename T>
+static void rs_tma_dispatch(int world, int grid, cudaStream_t stream, const PeerPtrs& P,
+                            int rank, int64_t slot_base, const ChunkTable& t) {
+  if (rs_tma_stages() == 6)
+    rs_tma_dispatch_s<T, 6>(world, grid, stream, P, rank, slot_base, t);
+  else
+    rs_tma_dispatch_s<T, 4>(world, grid, stream, P, rank, slot_base, t);
 }
 
 // DEFT_RS_IMPL=tma|ldg selects the SM-channel reduce-scatter (default tma: the
