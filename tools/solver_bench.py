@@ -10,7 +10,8 @@ Per fixture configuration (reference pkg/fixtures profiles, dual-link cluster):
     times measured in the build container are in BASELINE.md (8.4-31.6 s);
   * DP kernel time (CUDA events inside deft_solver_solve) and its algorithmic
     bytes (sum over placeable items of 2*ceil((cap'+1)/8)).
-Also a batched-throughput case: 1024 random problems (n=48, cap 1e6) per launch.
+Also the SURVEY 8d grid (n in {10, 25, 48, 551} x cap in {2.5e5, 1e6, 1e7}, w ~ U[1, cap/n],
+seed 0) single-problem and 256-per-launch, and 1024 random problems (n=48, cap 1e6) per launch.
 """
 import argparse
 import json
@@ -112,6 +113,32 @@ def main():
                      "dp_alg_bytes": counting.bytes,
                      "dp_achieved_gbs": round(counting.bytes / (kms / 1e3) / 1e9, 1) if kms else None})
         print(json.dumps(rows[-1]), flush=True)
+    # SURVEY 8d solver microbench grid: w ~ U[1, cap/n], n x cap, seed 0; one problem
+    # per call (latency) and 256 per launch (throughput), vs the C oracle on 1 core
+    rng = random.Random(0)
+    for n in (10, 25, 48, 551):
+        for cap in (250_000, 1_000_000, 10_000_000):
+            probs = [([rng.randint(1, max(1, cap // n)) for _ in range(n)], cap)
+                     for _ in range(256)]
+            assert solver.solve(probs[:4]) == O.subset_sum_c_batch(probs[:4])
+            k0 = solver.kernel_ms
+            t0 = time.perf_counter()
+            for pr in probs[:16]:
+                solver.solve([pr])
+            t_single = (time.perf_counter() - t0) / 16
+            k_single = (solver.kernel_ms - k0) / 16
+            k0 = solver.kernel_ms
+            solver.solve(probs)
+            k_batch = solver.kernel_ms - k0
+            t0 = time.perf_counter()
+            O.subset_sum_c_batch(probs[:8])
+            t_cpu = (time.perf_counter() - t0) / 8
+            nb = alg_bytes(probs)
+            print(json.dumps({"config": f"grid n={n} cap={cap}", "single_wall_ms":
+                              round(t_single * 1e3, 3), "single_kernel_ms": round(k_single, 4),
+                              "batch256_kernel_ms": round(k_batch, 3),
+                              "batch256_alg_gbs": round(nb / (k_batch / 1e3) / 1e9, 1),
+                              "oracle_cpu_ms_per_problem": round(t_cpu * 1e3, 3)}), flush=True)
     # batched throughput: many independent problems per launch
     rng = random.Random(0)
     probs = [([rng.randint(1, 40_000) for _ in range(48)], 1_000_000) for _ in range(1024)]
