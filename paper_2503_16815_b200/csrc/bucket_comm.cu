@@ -1090,7 +1090,7 @@ namespace deft {
 // "start" placement uses still streams at NVLink rate.
 // ============================================================================
 constexpr int kUpdTmaThreads = 256;
-constexpr int kUpdTmaStages = 3;
+constexpr int kUpdTmaStagesDefault = 3;   // DEFT_UPDATE_TMA_STAGES: 3 or 6
 constexpr int kUpdChunk = 2048;  // elements per chunk (multiple of 8)
 
 __device__ __forceinline__ void tma_store_1d(void* dst_gmem, const void* src_smem,
@@ -1110,7 +1110,7 @@ __device__ __forceinline__ void tma_store_wait_all() {
 }
 
 
-template <typename T, int W>
+template <typename T, int W, int kUpdTmaStages>
 __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
     PeerPtrs P, int rank, int64_t slot_base, ChunkTable t, float lr, float momentum,
     float scale, float* __restrict__ mom) {
@@ -1225,6 +1225,14 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
   peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 2u);
 }
 
+static int upd_tma_stages() {
+  static int v = [] {
+    const char* e = getenv("DEFT_UPDATE_TMA_STAGES");
+    return e && atoi(e) == 6 ? 6 : kUpdTmaStagesDefault;
+  }();
+  return v;
+}
+
 bool launch_update_allgather_tma(const PeerPtrs& P, int rank, int world, int dtype,
                                  int64_t slot_base, int32_t count, const int64_t* offsets,
                                  const int64_t* numels, float lr, float momentum,
@@ -1244,20 +1252,23 @@ bool launch_update_allgather_tma(const PeerPtrs& P, int rank, int world, int dty
     int grid = comm_grid_for((total_elems + world - 1) / world);
     if (max_blocks > 0 && grid > max_blocks) grid = max_blocks;
     const size_t esz = dtype == 0 ? 4 : 2;
-    const size_t smem = (size_t)kUpdTmaStages *
+    const int stages = upd_tma_stages();
+    const size_t smem = (size_t)stages *
                         (kUpdChunk * esz + 2 * kUpdChunk * 4 + (dtype == 0 ? 0 : kUpdChunk * esz));
+#define DEFT_UPT_LAUNCH(TT, WW, SS)                                                            \
+  {                                                                                            \
+    cudaFuncSetAttribute(update_allgather_tma_kernel<TT, WW, SS>,                              \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
+    update_allgather_tma_kernel<TT, WW, SS><<<grid, kUpdTmaThreads, smem, stream>>>(           \
+        P, rank, slot_base, t, lr, momentum, grad_scale, mom);                                 \
+  }
 #define DEFT_UPT_CASE(WW)                                                                      \
   case WW:                                                                                     \
     if (dtype == 0) {                                                                          \
-      cudaFuncSetAttribute(update_allgather_tma_kernel<float, WW>,                             \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
-      update_allgather_tma_kernel<float, WW><<<grid, kUpdTmaThreads, smem, stream>>>(          \
-          P, rank, slot_base, t, lr, momentum, grad_scale, mom);                               \
+      if (stages == 6) DEFT_UPT_LAUNCH(float, WW, 6) else DEFT_UPT_LAUNCH(float, WW, 3)        \
     } else {                                                                                   \
-      cudaFuncSetAttribute(update_allgather_tma_kernel<__nv_bfloat16, WW>,                     \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
-      update_allgather_tma_kernel<__nv_bfloat16, WW><<<grid, kUpdTmaThreads, smem, stream>>>(  \
-          P, rank, slot_base, t, lr, momentum, grad_scale, mom);                               \
+      if (stages == 6) DEFT_UPT_LAUNCH(__nv_bfloat16, WW, 6)                                   \
+      else DEFT_UPT_LAUNCH(__nv_bfloat16, WW, 3)                                               \
     }                                                                                          \
     break;
     switch (world) {
@@ -1266,6 +1277,7 @@ bool launch_update_allgather_tma(const PeerPtrs& P, int rank, int world, int dty
       default: break;
     }
 #undef DEFT_UPT_CASE
+#undef DEFT_UPT_LAUNCH
     count_launch();
   }
   return true;
