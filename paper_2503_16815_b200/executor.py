@@ -23,6 +23,10 @@ for every event of decision (s-2, backward).  Compute never waits for a
 transfer; it only waits, at each forward start, for the (short) update
 kernels due at that version -- the zero-stall property of simulator.py:12-14.
 
+The reference's synchronous baseline schedules (``scheme="wfbp"`` /
+``"priority"``, scheduler.py:386-418) run on the same machinery with their
+update events visible from t+1 (planner lag 0 / 1).
+
 Memory (B200, 180 GB HBM): the flat fp32 parameter buffer (output-side
 bucket first, every module parameter is a view into it), a momentum buffer
 and ``n_slots`` gradient group slots, all symmetric (CUDA-IPC mapped by every
