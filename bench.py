@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--scheme", default="deft", choices=["deft", "wfbp", "priority"],
                     help="schedule run on the executor: DeFT, or one of the reference's "
                          "synchronous baselines (scheduler.py:386-418) on the same kernels")
+    ap.add_argument("--start-grouping", default="size", choices=["size", "timed"],
+                    help="how start-placement updates are grouped into launches")
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs")
     ap.add_argument("--bucket-mb", type=float, default=None,
                     help="partition size in MB of fp32 (default: the reference's 6.5M params)")
@@ -525,6 +527,7 @@ def main():
                        cuda_graphs=False if args.eager else "auto",
                        update_placement=args.update_placement,
                        update_blocks=args.update_blocks, scheme=args.scheme,
+                       start_grouping=args.start_grouping,
                        autocast_dtype=None if args.model == "gpt2" else torch.bfloat16,
                        partition=D.PartitionConfig(partition_size=psize, mu=1.0))
     ddp = D.DeftDataParallel(model, cfg)

@@ -177,3 +177,45 @@ def release_runs(transfers) -> list[tuple[int, int, list[int]]]:
             out.append(cur)
         cur[2].append(bidx)
     return out
+
+
+def start_groups_timed(bucket_sizes: list[int], forward_us: list[float],
+                       update_us_per_elem: float, launch_us: float,
+                       max_groups: int) -> list[list[int]]:
+    """"start" placement from the measured profile: the fewest update launches
+    such that each group's update (run back to back on the update stream,
+    `launch_us` + size x `update_us_per_elem` each) completes before the forward
+    reaches the group's first bucket (forward order = input side first; bucket
+    i's forward starts after the forward time of the buckets before it).  The
+    first group is the input-side bucket alone (the forward waits for it
+    whatever its size).  A bucket that cannot be ready in time starts its own
+    group.  Returns bucket indices, like `start_groups`."""
+    order = list(range(len(bucket_sizes) - 1, -1, -1))
+    if not order:
+        return []
+    arrive, t = [], 0.0
+    for b in order:
+        arrive.append(t)
+        t += forward_us[b]
+    groups = [[order[0]]]
+    done = launch_us + bucket_sizes[order[0]] * update_us_per_elem
+    i = 1
+    while i < len(order):
+        j, size = i, 0
+        # extend while the group's completion precedes the forward's arrival at
+        # its first bucket (the binding one: arrival times only grow)
+        while j < len(order):
+            cand = done + launch_us + (size + bucket_sizes[order[j]]) * update_us_per_elem
+            if j > i and cand > arrive[i]:
+                break
+            size += bucket_sizes[order[j]]
+            j += 1
+            if cand > arrive[i]:          # even alone it is late: keep it alone
+                break
+        if len(groups) == max_groups - 1:  # launch cap: the rest in one group
+            j = len(order)
+            size = sum(bucket_sizes[order[k]] for k in range(i, j))
+        groups.append(order[i:j])
+        done += launch_us + size * update_us_per_elem
+        i = j
+    return groups

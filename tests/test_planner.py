@@ -199,3 +199,19 @@ def test_release_runs_keep_per_link_plan_order():
         assert [b for l, _, bl in runs if l == link for b in bl] == \
             [b for l, _, b in tr if l == link]
     assert release_runs([]) == []
+
+
+def test_start_groups_timed():
+    from paper_2503_16815_b200.planner import start_groups_timed
+    sizes = [4_000, 100_000, 2_000, 2_000, 2_000]      # output side first
+    fwd = [10.0, 50.0, 400.0, 400.0, 400.0]            # input-side layers dominate
+    # fast updates: the input-side bucket alone, then everything in one launch
+    g = start_groups_timed(sizes, fwd, 1e-3, 5.0, 8)
+    assert g[0] == [4] and len(g) == 2
+    assert [b for grp in g for b in grp] == [4, 3, 2, 1, 0]
+    # slow updates: each group must complete before the forward reaches it
+    g = start_groups_timed(sizes, fwd, 1e-1, 5.0, 8)
+    assert [b for grp in g for b in grp] == [4, 3, 2, 1, 0] and len(g) > 2
+    # launch cap honoured
+    assert len(start_groups_timed(sizes, fwd, 10.0, 5.0, 3)) <= 3
+    assert start_groups_timed([], [], 1e-3, 5.0, 8) == []
