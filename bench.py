@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--scheme", default="deft", choices=["deft", "wfbp", "priority"],
                     help="schedule run on the executor: DeFT, or one of the reference's "
                          "synchronous baselines (scheduler.py:386-418) on the same kernels")
-    ap.add_argument("--start-grouping", default="size", choices=["size", "timed"],
+    ap.add_argument("--start-grouping", default="auto", choices=["auto", "size", "timed"],
                     help="how start-placement updates are grouped into launches")
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs")
     ap.add_argument("--bucket-mb", type=float, default=None,

@@ -86,8 +86,9 @@ class DeftConfig:
     update_blocks: int = 0
     start_groups: int = 8                   # max update launches per event with "start"
     # "timed": as few launches as the measured forward can hide (planner.start_groups_timed);
-    # "size": a small first group, then similar sizes (planner.start_groups)
-    start_grouping: str = "size"
+    # "size": a small first group, then similar sizes (planner.start_groups);
+    # "auto": timed when it predicts no forward wait, else size
+    start_grouping: str = "auto"
     # "deft" (delayed updates) or one of the reference's synchronous baselines on
     # the same kernels (scheduler.py:386-418): "wfbp" (every bucket at its own
     # backward end, measured buckets) / "priority" (partition_by_size blocks,
@@ -537,16 +538,19 @@ class DeftDataParallel:
     def _start_groups(self) -> list[list[int]]:
         if getattr(self, "_groups_cache", None) is None:
             sizes = [b.hi - b.lo for b in self.buckets]
-            if self.cfg.start_grouping == "timed" and self.schedule_profile is not None:
+            groups = None
+            if self.cfg.start_grouping in ("auto", "timed") and self.schedule_profile is not None:
                 # update-stream cost model under the start budget (conservative:
                 # measured 300-630 GB/s isolated, less beside the forward)
                 esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
                 per_elem_us = esz * max(1, self.world - 1) / max(1, self.world) / 200e3
                 fwd = [b.forward_us for b in self.schedule_profile.buckets]
-                self._groups_cache = start_groups_timed(sizes, fwd, per_elem_us, 20.0,
-                                                        self.cfg.start_groups)
-            else:
-                self._groups_cache = start_groups(sizes, self.cfg.start_groups)
+                rep: dict = {}
+                groups = start_groups_timed(sizes, fwd, per_elem_us, 20.0,
+                                            self.cfg.start_groups, rep)
+                if self.cfg.start_grouping == "auto" and not rep["feasible"]:
+                    groups = None   # the forward cannot hide them: size-based groups
+            self._groups_cache = groups or start_groups(sizes, self.cfg.start_groups)
         return self._groups_cache
 
     def _updates_at_start(self, comp, due):

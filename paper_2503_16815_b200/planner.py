@@ -181,7 +181,7 @@ def release_runs(transfers) -> list[tuple[int, int, list[int]]]:
 
 def start_groups_timed(bucket_sizes: list[int], forward_us: list[float],
                        update_us_per_elem: float, launch_us: float,
-                       max_groups: int) -> list[list[int]]:
+                       max_groups: int, report: dict | None = None) -> list[list[int]]:
     """"start" placement from the measured profile: the fewest update launches
     such that each group's update (run back to back on the update stream,
     `launch_us` + size x `update_us_per_elem` each) completes before the forward
@@ -191,6 +191,7 @@ def start_groups_timed(bucket_sizes: list[int], forward_us: list[float],
     whatever its size).  A bucket that cannot be ready in time starts its own
     group.  Returns bucket indices, like `start_groups`."""
     order = list(range(len(bucket_sizes) - 1, -1, -1))
+    feasible = True
     if not order:
         return []
     arrive, t = [], 0.0
@@ -211,11 +212,15 @@ def start_groups_timed(bucket_sizes: list[int], forward_us: list[float],
             size += bucket_sizes[order[j]]
             j += 1
             if cand > arrive[i]:          # even alone it is late: keep it alone
+                feasible = False
                 break
-        if len(groups) == max_groups - 1:  # launch cap: the rest in one group
-            j = len(order)
+        if len(groups) == max_groups - 1 and j < len(order):  # launch cap: the rest
+            j = len(order)                                     # in one group
             size = sum(bucket_sizes[order[k]] for k in range(i, j))
+            feasible = feasible and done + launch_us + size * update_us_per_elem <= arrive[i]
         groups.append(order[i:j])
         done += launch_us + size * update_us_per_elem
         i = j
+    if report is not None:
+        report["feasible"] = feasible   # no forward wait predicted after the first group
     return groups

@@ -209,8 +209,12 @@ def test_start_groups_timed():
     g = start_groups_timed(sizes, fwd, 1e-3, 5.0, 8)
     assert g[0] == [4] and len(g) == 2
     assert [b for grp in g for b in grp] == [4, 3, 2, 1, 0]
+    rep = {}
+    start_groups_timed(sizes, fwd, 1e-3, 5.0, 8, rep)
+    assert rep["feasible"]
     # slow updates: each group must complete before the forward reaches it
-    g = start_groups_timed(sizes, fwd, 1e-1, 5.0, 8)
+    g = start_groups_timed(sizes, fwd, 1e-1, 5.0, 8, rep)
+    assert not rep["feasible"]
     assert [b for grp in g for b in grp] == [4, 3, 2, 1, 0] and len(g) > 2
     # launch cap honoured
     assert len(start_groups_timed(sizes, fwd, 10.0, 5.0, 3)) <= 3
