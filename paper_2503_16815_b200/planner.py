@@ -194,6 +194,10 @@ def start_groups_timed(bucket_sizes: list[int], forward_us: list[float],
     feasible = True
     if not order:
         return []
+    if max_groups <= 1:
+        if report is not None:
+            report["feasible"] = len(order) == 1
+        return [order]
     arrive, t = [], 0.0
     for b in order:
         arrive.append(t)
@@ -214,7 +218,7 @@ def start_groups_timed(bucket_sizes: list[int], forward_us: list[float],
             if cand > arrive[i]:          # even alone it is late: keep it alone
                 feasible = False
                 break
-        if len(groups) == max_groups - 1 and j < len(order):  # launch cap: the rest
+        if len(groups) >= max_groups - 1 and j < len(order):  # launch cap: the rest
             j = len(order)                                     # in one group
             size = sum(bucket_sizes[order[k]] for k in range(i, j))
             feasible = feasible and done + launch_us + size * update_us_per_elem <= arrive[i]
