@@ -3,8 +3,6 @@ reference's own property tests (test_knapsack.py:81-91, 176-187; test_partition.
 test_profiles.py:115-128) plus the executor planner's invariants on random
 schedules.  The DP runs through the CPU oracle backend here (no GPU); the same
 wrappers run the sm_100a kernel in the GPU tests."""
-import math
-
 import pytest
 from hypothesis import given, settings
 from hypothesis import strategies as st
@@ -158,3 +156,41 @@ def test_release_runs_preserve_per_link_order(transfers):
     for link in {l for l, _, _ in transfers}:
         slots = [s for l, s, _ in runs if l == link]
         assert all(a != b for a, b in zip(slots, slots[1:]))
+
+
+@given(st.integers(1, 4096), st.integers(1, 4096))
+@settings(max_examples=60, deadline=None)
+def test_larger_batch_never_worse(b1, b2):
+    """preserver.py:97-112 via the product's restatement: the expected next state
+    is monotone non-increasing in the batch size (reference
+    test_preserver.py:66-75), and never below the optimum."""
+    p = D.WalkParams(s0=0.3, s_star=0.0, eta=0.01, mu_t=1.0, sigma_t=30.0)
+    lo, hi = sorted((b1, b2))
+    assert D.expected_next_state(0.3, hi, p) <= D.expected_next_state(0.3, lo, p) + 1e-12
+    q = D.WalkParams(s0=0.2, s_star=0.05, eta=0.1, mu_t=5.0, sigma_t=2.0)
+    assert D.expected_next_state(0.2, lo, q) >= q.s_star
+
+
+@given(st.integers(4, 24), st.integers(100, 3000), st.floats(1.0, 1.5))
+@settings(max_examples=30, deadline=None)
+def test_sequence_from_merge_counts_equals_extract(n, comm_us, mult):
+    """The lazy K5 path builds the preserver's batch sequence from the update
+    events' merge counts alone; it must equal extract_batch_sequence of the full
+    decision stream (preserver.py:137-168)."""
+    from paper_2503_16815_b200.preserver import sequence_from_merge_counts
+    prof = D.ModelProfile(name="u", buckets=tuple(
+        D.BucketProfile(i + 1, 1000, 3600 // n, 7200 // n, comm_us) for i in range(n)),
+        batch_size=32)
+    cluster = D.ClusterSpec(links=(D.LinkSpec("fast"), D.LinkSpec("slow", 1.65)))
+    iters = 120
+    decisions = D.DeftScheduler(prof, cluster, mult).run(iters)
+    sched = D.Schedule("deft", prof, cluster, decisions, True, iters)
+    ks = [u.merge_count for d in decisions for u in d.update_events]
+    try:
+        want = D.extract_batch_sequence(sched)
+    except D.DeftError as e:
+        with pytest.raises(type(e)):
+            sequence_from_merge_counts(ks, prof.batch_size, iters)
+        return
+    got = sequence_from_merge_counts(ks, prof.batch_size, iters)
+    assert got == want
