@@ -139,6 +139,14 @@ deft_status_t deft_comm_create(int32_t rank, int32_t world, void* const* grads,
 deft_status_t deft_comm_destroy(deft_comm* c);
 /* CTA budget of the update kernels (0 = default); must be equal on every rank. */
 deft_status_t deft_comm_set_update_blocks(deft_comm* c, int32_t blocks);
+/* grid_cap (>= 0; 0 = none): CTA cap of every kernel that meets its peers in a
+ * barrier -- a loopback world (W ranks in one process on ONE GPU, peer
+ * pointers local) sets about 148/(2W) so that all ranks' blocks are
+ * co-resident.  spin_timeout_ms (>= 0; 0 = unbounded; default
+ * DEFT_SPIN_TIMEOUT_MS or 120000): a barrier spin longer than this traps
+ * instead of hanging the GPU.  A negative argument keeps the current value.
+ * Both must be equal on every rank. */
+deft_status_t deft_comm_configure(deft_comm* c, int32_t grid_cap, int64_t spin_timeout_ms);
 
 /* grad_dtype codes */
 #define DEFT_DTYPE_F32 0
@@ -211,6 +219,19 @@ deft_status_t deft_sgd_momentum_update_multi(const void* d_grad, int32_t grad_dt
 deft_status_t deft_gather_segments(void* d_dst, const void* const* d_srcs,
                                    const int64_t* dst_offsets, const int64_t* byte_lens,
                                    int32_t count, int64_t ce_min_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Streams and hardware work queues (loopback worlds, loopback.py).
+ * deft_stream_create: a non-blocking stream of the given priority.
+ * deft_stream_alias_probe: *aliased = 1 if work on stream_b issued after a
+ * blocked entry of stream_a waits for it (the two share a hardware queue),
+ * measured with a bounded spin of timeout_us; the blocked entry is a kernel
+ * (mode 0) or a device-to-device copy (mode 1); synchronizes both streams.
+ * ------------------------------------------------------------------------ */
+deft_status_t deft_stream_create(int32_t priority, void** out);
+deft_status_t deft_stream_destroy(void* stream);
+deft_status_t deft_stream_alias_probe(void* stream_a, void* stream_b, int32_t timeout_us,
+                                      int32_t mode, int32_t* aliased);
 
 #ifdef __cplusplus
 }

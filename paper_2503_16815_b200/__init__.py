@@ -39,4 +39,7 @@ def __getattr__(name):
     if name in ("DeftDataParallel", "DeftConfig"):
         from . import executor
         return getattr(executor, name)
+    if name in ("LoopbackWorld", "LoopbackRank"):
+        from . import loopback
+        return getattr(loopback, name)
     raise AttributeError(name)

@@ -25,10 +25,11 @@ EXPORTED = (
     "deft_sched_carry_bytes",
     "deft_mem_alloc", "deft_mem_free", "deft_mem_open", "deft_mem_close",
     "deft_comm_flag_bytes", "deft_comm_create", "deft_comm_destroy",
-    "deft_comm_set_update_blocks",
+    "deft_comm_set_update_blocks", "deft_comm_configure",
     "deft_bucket_reduce_scatter", "deft_bucket_reduce_scatter_multi", "deft_bucket_update",
     "deft_bucket_update_multi",
     "deft_sgd_momentum_update", "deft_sgd_momentum_update_multi", "deft_gather_segments",
+    "deft_stream_create", "deft_stream_destroy", "deft_stream_alias_probe",
 )
 
 DTYPE_F32, DTYPE_BF16 = 0, 1
@@ -73,6 +74,10 @@ def _declare(lib):
                                      c_i32, c_i32, P(c_vp)]),
         "deft_comm_destroy": (c_i32, [c_vp]),
         "deft_comm_set_update_blocks": (c_i32, [c_vp, c_i32]),
+        "deft_comm_configure": (c_i32, [c_vp, c_i32, c_i64]),
+        "deft_stream_create": (c_i32, [c_i32, P(c_vp)]),
+        "deft_stream_destroy": (c_i32, [c_vp]),
+        "deft_stream_alias_probe": (c_i32, [c_vp, c_vp, c_i32, c_i32, P(c_i32)]),
         "deft_bucket_reduce_scatter": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i64, c_vp]),
         "deft_bucket_reduce_scatter_multi": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_vp, c_vp,
                                                      c_vp]),

@@ -62,13 +62,17 @@ class BucketComm:
     """Per-rank communicator over the symmetric gradient arena / params / flags."""
 
     def __init__(self, rank: int, world: int, n_slots: int, slot_elems: int,
-                 grad_dtype: torch.dtype, device: torch.device, group=None):
+                 grad_dtype: torch.dtype, device: torch.device, group=None,
+                 connect: bool = True):
+        """``connect=False`` only allocates this rank's regions; a loopback
+        world (loopback.py) maps every rank's pointers and calls ``_connect``."""
         self.rank, self.world = rank, world
+        self.group = group
         self.n_slots, self.slot_elems = n_slots, slot_elems
         self.grad_dtype = grad_dtype
         self.device = device
         esz = 2 if grad_dtype == torch.bfloat16 else 4
-        ipc = world > 1
+        ipc = world > 1 and connect
         # slots start 256-byte aligned (the kernels' vector and TMA bulk accesses
         # are aligned relative to the slot base)
         self.slot_stride = -(-slot_elems // 128) * 128
@@ -86,19 +90,35 @@ class BucketComm:
         fbytes = int(_native.lib().deft_comm_flag_bytes(world))
         self.flags, self._f = region_tensor(fbytes, torch.uint8, ipc, device)
         self._opened: list[c_vp] = []
+        self._h = None
+        self.loopback = not connect
+        if not connect:
+            return
         if world > 1:
             maps = self._exchange(group)
         else:
-            maps = PeerMaps([self._g.ptr.value], [self._p.ptr.value], [self._f.ptr.value])
-        arr = lambda xs: (c_vp * world)(*xs)  # noqa: E731
+            maps = self.own_maps()
+        self._connect(maps)
+
+    def own_maps(self) -> PeerMaps:
+        return PeerMaps([self._g.ptr.value], [self._p.ptr.value], [self._f.ptr.value])
+
+    def _connect(self, maps: PeerMaps) -> None:
+        arr = lambda xs: (c_vp * self.world)(*xs)  # noqa: E731
         h = c_vp()
         check(_native.lib().deft_comm_create(
-            rank, world, arr(maps.grads), arr(maps.params), arr(maps.flags),
+            self.rank, self.world, arr(maps.grads), arr(maps.params), arr(maps.flags),
             c_vp(self.master.data_ptr() if self.master is not None else None), self.slot_stride,
-            n_slots,
-            DTYPE_BF16 if grad_dtype == torch.bfloat16 else DTYPE_F32, ctypes.byref(h)),
+            self.n_slots,
+            DTYPE_BF16 if self.grad_dtype == torch.bfloat16 else DTYPE_F32, ctypes.byref(h)),
             "deft_comm_create")
         self._h = h
+
+    def configure(self, grid_cap: int = -1, spin_timeout_ms: int = -1) -> None:
+        """deft_comm_configure: CTA cap of the peer-barrier kernels and the
+        barrier spin timeout (negative = unchanged); equal on every rank."""
+        check(_native.lib().deft_comm_configure(self._h, int(grid_cap), int(spin_timeout_ms)),
+              "deft_comm_configure")
 
     def _exchange(self, group) -> PeerMaps:
         import torch.distributed as dist
@@ -171,9 +191,15 @@ class BucketComm:
             self._h, slot, n, offs, lens, lr, momentum, scale, c_vp(mom.data_ptr()),
             c_vp(stream.cuda_stream)), "deft_bucket_update_multi")
 
-    def close(self) -> None:
+    def close(self, barrier: bool = True) -> None:
         if getattr(self, "_h", None) is not None:
             torch.cuda.synchronize(self.device)
+            if barrier and self.world > 1 and not self.loopback:
+                # a peer's last kernels may still read our gradient slots / write
+                # our parameters over NVLink: nobody unmaps before everyone is done
+                import torch.distributed as dist
+                if dist.is_initialized():
+                    dist.barrier(group=self.group)
             _native.lib().deft_comm_destroy(self._h)
             self._h = None
             for p in self._opened:
@@ -182,7 +208,7 @@ class BucketComm:
 
     def __del__(self):
         try:
-            self.close()
+            self.close(barrier=False)
         except Exception:
             pass
 

@@ -24,6 +24,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <vector>
@@ -91,7 +92,15 @@ __device__ __forceinline__ uint32_t take_epochs(const PeerPtrs& P, int rank, int
   return s_epoch;
 }
 
-// Block-level barrier with the same-index block on every rank.
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Block-level barrier with the same-index block on every rank.  The spin is
+// bounded by P.spin_timeout_ns: a peer block that never arrives (a launch whose
+// blocks cannot all be resident, a rank that died) traps with a message.
 __device__ __forceinline__ void peer_block_barrier(const PeerPtrs& P, int rank, int world,
                                                    int set, int block, uint32_t value) {
   __threadfence_system();
@@ -101,8 +110,16 @@ __device__ __forceinline__ void peer_block_barrier(const PeerPtrs& P, int rank, 
     const int64_t base = ((int64_t)set * kMaxCommBlocks + block) * kMaxWorld;
     st_release_sys(P.flags[peer] + base + rank, value);
     const uint32_t* mine = P.flags[rank] + base + peer;
+    const uint64_t limit = P.spin_timeout_ns;
+    const uint64_t t0 = limit ? global_ns() : 0;
     // wrap-safe "mine >= value"
-    while ((int32_t)(ld_acquire_sys(mine) - value) < 0) {
+    uint32_t seen;
+    while ((int32_t)((seen = ld_acquire_sys(mine)) - value) < 0) {
+      if (limit && global_ns() - t0 > limit) {
+        printf("deft: peer barrier timeout: rank %d waits for rank %d (set %d block %d, "
+               "epoch %u, seen %u)\n", rank, peer, set, block, value, seen);
+        __trap();
+      }
     }
   }
   __syncthreads();
@@ -300,7 +317,7 @@ cudaError_t launch_reduce_scatter_sm(const PeerPtrs& P, int rank, int world, int
     return cudaGetLastError();
   const int align = dtype == 0 ? 4 : 8;
   const ShardRange sh = shard_of(offset, numel, rank, world, align);
-  const int grid = comm_grid_for((numel + world - 1) / world);
+  const int grid = cap_grid(P, comm_grid_for((numel + world - 1) / world));
   if (dtype == 0)
     rs_dispatch<float>(world, grid, stream, P, rank, slot_base, sh.lo, sh.hi);
   else
@@ -478,6 +495,7 @@ cudaError_t launch_update_allgather(const PeerPtrs& P, int rank, int world, int 
   const ShardRange sh = shard_of(offset, numel, rank, world, dtype == 0 ? 4 : 8);
   int grid = comm_grid_for((numel + world - 1) / world);
   if (max_blocks > 0 && grid > max_blocks) grid = max_blocks;
+  grid = cap_grid(P, grid);
   if (dtype == 0)
     upd_dispatch<float>(world, grid, stream, P, rank, slot_base, sh.lo, sh.hi, lr, momentum,
                         grad_scale, mom);
@@ -781,6 +799,7 @@ cudaError_t launch_update_allgather_multi(const PeerPtrs& P, int rank, int world
     // identical on every rank: depends on the bucket sizes, not on this rank's shards
     int grid = comm_grid_for((total_elems + world - 1) / world);
     if (max_blocks > 0 && grid > max_blocks) grid = max_blocks;
+    grid = cap_grid(P, grid);
 #define DEFT_UPM_CASE(WW)                                                                   \
   case WW:                                                                                  \
     if (dtype == 0)                                                                         \
@@ -910,6 +929,9 @@ __global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
   constexpr int64_t kChunk = rs_tma_chunk<T, W>();
   const uint32_t epoch = take_epochs(P, rank, kBarrierRS, 1u) + 1u;
   peer_block_barrier(P, rank, W, kBarrierRS, blockIdx.x, epoch);
+  // the barrier's acquire is a generic-proxy operation; the peers' gradient
+  // bytes are read by the async proxy (cp.async.bulk): order the two
+  if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
   const T* src[W];
 #pragma unroll
   for (int k = 0; k < W; ++k) src[k] = reinterpret_cast<const T*>(P.grads[k]) + slot_base;
@@ -1059,6 +1081,7 @@ bool launch_reduce_scatter_tma_multi(const PeerPtrs& P, int rank, int world, int
     int grid = (int)((per + 32767) / 32768);
     if (grid < 1) grid = 1;
     if (grid > rs_tma_blocks()) grid = rs_tma_blocks();
+    grid = cap_grid(P, grid);
     if (dtype == 0)
       rs_tma_dispatch<float>(world, grid, stream, P, rank, slot_base, t);
     else
@@ -1125,6 +1148,8 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
 
   const uint32_t epoch = take_epochs(P, rank, kBarrierUpdate, 2u);
   peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 1u);
+  // generic acquire -> async-proxy (bulk copy) accesses of global memory
+  if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
   const T* g = reinterpret_cast<const T*>(P.grads[rank]) + slot_base;
   float* ref = kMaster ? P.master : reinterpret_cast<float*>(P.params[rank]);
   T* dst[W];
@@ -1251,6 +1276,7 @@ bool launch_update_allgather_tma(const PeerPtrs& P, int rank, int world, int dty
     for (int k = 0; k < t.count; ++k) total_elems += numels[s0 + k];
     int grid = comm_grid_for((total_elems + world - 1) / world);
     if (max_blocks > 0 && grid > max_blocks) grid = max_blocks;
+    grid = cap_grid(P, grid);
     const size_t esz = dtype == 0 ? 4 : 2;
     const int stages = upd_tma_stages();
     const size_t smem = (size_t)stages *

@@ -1,6 +1,7 @@
 // C-ABI of libdeft_b200.so (declared in include/deft_b200.h).
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -27,6 +28,8 @@ static deft_status_t fail(deft_status_t code, const std::string& msg) {
 static deft_status_t cuda_fail(cudaError_t e, const char* where) {
   return fail(DEFT_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
+// for the other translation units (streams.cu)
+deft_status_t deft_fail_cuda(cudaError_t e, const char* where) { return cuda_fail(e, where); }
 #define DEFT_CUDA(call)                                  \
   do {                                                   \
     cudaError_t e_ = (call);                             \
@@ -327,6 +330,14 @@ extern "C" size_t deft_comm_flag_bytes(int32_t world) {
   return (size_t)kNumBarrierSets * kMaxCommBlocks * (kMaxWorld + 1) * sizeof(uint32_t);
 }
 
+// DEFT_SPIN_TIMEOUT_MS (default 120 s; 0 = unbounded): longest wait of a peer
+// barrier before the kernel traps
+static uint64_t default_spin_timeout_ns() {
+  const char* e = getenv("DEFT_SPIN_TIMEOUT_MS");
+  const long long ms = e ? atoll(e) : 120000LL;
+  return ms > 0 ? (uint64_t)ms * 1000000ull : 0ull;
+}
+
 extern "C" deft_status_t deft_comm_create(int32_t rank, int32_t world, void* const* grads,
                                           void* const* params, void* const* flags,
                                           float* d_master, int64_t slot_elems, int32_t n_slots,
@@ -339,6 +350,8 @@ extern "C" deft_status_t deft_comm_create(int32_t rank, int32_t world, void* con
     return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_comm_create: bf16 parameters need an fp32 master");
   deft_comm* c = new deft_comm();
   c->P.master = grad_dtype == DEFT_DTYPE_BF16 ? d_master : nullptr;
+  c->P.grid_cap = 0;
+  c->P.spin_timeout_ns = default_spin_timeout_ns();
   c->rank = rank;
   c->world = world;
   c->dtype = grad_dtype;
@@ -376,6 +389,15 @@ extern "C" deft_status_t deft_comm_set_update_blocks(deft_comm* c, int32_t block
   if (!c || blocks < 0 || blocks > kMaxCommBlocks)
     return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_comm_set_update_blocks");
   c->update_blocks = blocks;
+  return DEFT_OK;
+}
+
+extern "C" deft_status_t deft_comm_configure(deft_comm* c, int32_t grid_cap,
+                                             int64_t spin_timeout_ms) {
+  if (!c || grid_cap > kMaxCommBlocks)
+    return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_comm_configure");
+  if (grid_cap >= 0) c->P.grid_cap = grid_cap;
+  if (spin_timeout_ms >= 0) c->P.spin_timeout_ns = (uint64_t)spin_timeout_ms * 1000000ull;
   return DEFT_OK;
 }
 

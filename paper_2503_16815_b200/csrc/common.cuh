@@ -44,7 +44,19 @@ struct PeerPtrs {
   void* params[kMaxWorld];   // same dtype as the gradients (fp32 or bf16)
   uint32_t* flags[kMaxWorld];
   float* master;             // this rank's fp32 master copy when params are bf16, else null
+  // CTA cap of every kernel that meets its peers in a barrier (0 = none).  A
+  // loopback world (W ranks on ONE GPU) sets it so that all ranks' blocks of a
+  // barrier kernel are co-resident.  Equal on every rank (grids must match).
+  int32_t grid_cap;
+  // a barrier spin longer than this traps (0 = unbounded): a peer that never
+  // arrives becomes a loud kernel fault instead of a hung GPU
+  uint64_t spin_timeout_ns;
 };
+
+// grid of a peer-barrier kernel after the communicator's cap
+__host__ inline int cap_grid(const PeerPtrs& P, int grid) {
+  return (P.grid_cap > 0 && grid > P.grid_cap) ? P.grid_cap : grid;
+}
 
 struct ShardRange {
   int64_t lo, hi;  // absolute element range [lo, hi) of this rank's shard

@@ -116,9 +116,16 @@ class DeftDataParallel:
         self.module = module
         self.group = process_group
         dist = torch.distributed
-        self.world = dist.get_world_size(process_group) if dist.is_initialized() else 1
-        self.rank = dist.get_rank(process_group) if dist.is_initialized() else 0
-        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        # a LoopbackRank (loopback.py): W ranks of one process on one GPU
+        from .loopback import LoopbackRank
+        self.loopback = process_group if isinstance(process_group, LoopbackRank) else None
+        if self.loopback is not None:
+            self.world, self.rank = self.loopback.world, self.loopback.rank
+        else:
+            self.world = dist.get_world_size(process_group) if dist.is_initialized() else 1
+            self.rank = dist.get_rank(process_group) if dist.is_initialized() else 0
+        self.device = device or (self.loopback.device if self.loopback is not None else
+                                 torch.device("cuda", torch.cuda.current_device()))
         self.placement = self.cfg.update_placement
         if self.placement == "auto":
             self.placement = "end" if self.world == 1 else "start"
@@ -139,15 +146,24 @@ class DeftDataParallel:
         # gradients (and the symmetric parameter copies) carry the parameter dtype;
         # bf16 models get an fp32 master inside the update kernel
         self.cfg.grad_dtype = next(iter(dtypes))
-        self.comm = BucketComm(self.rank, self.world, self.cfg.n_slots, self.total,
-                               self.cfg.grad_dtype, self.device, process_group)
+        if self.loopback is not None:
+            self.comm = self.loopback.comm(self.cfg.n_slots, self.total, self.cfg.grad_dtype)
+        else:
+            self.comm = BucketComm(self.rank, self.world, self.cfg.n_slots, self.total,
+                                   self.cfg.grad_dtype, self.device, process_group)
         self.mom = torch.zeros(self.total, dtype=torch.float32, device=self.device)
         self._bind_params()
-        self.compute_stream = torch.cuda.Stream(self.device)
-        prio_lo, prio_hi = torch.cuda.Stream.priority_range()
-        self.update_stream = torch.cuda.Stream(self.device, priority=prio_hi)
-        # store path: bucket gathers run here, off the backward's critical path
-        self.gather_stream = torch.cuda.Stream(self.device)
+        if self.loopback is not None:
+            # two streams per rank; links, gathers and updates share one in-order
+            # comm stream (identical issue order on every rank: loopback.py)
+            self.compute_stream = self.loopback.compute_stream
+            self.update_stream = self.gather_stream = self.loopback.comm_stream
+        else:
+            self.compute_stream = torch.cuda.Stream(self.device)
+            prio_lo, prio_hi = torch.cuda.Stream.priority_range()
+            self.update_stream = torch.cuda.Stream(self.device, priority=prio_hi)
+            # store path: bucket gathers run here, off the backward's critical path
+            self.gather_stream = torch.cuda.Stream(self.device)
         self.link_streams: list[torch.cuda.Stream] = []
         self.profile: ModelProfile | None = None
         self.schedule_profile: ModelProfile | None = None
@@ -174,8 +190,19 @@ class DeftDataParallel:
                 p.data = view
                 self.offsets.append(off)
                 off += n
-            if self.world > 1:
+            # every rank starts from rank 0's parameters and module buffers
+            # (BatchNorm running statistics; like DDP's broadcast_buffers)
+            buffers = [b for b in self.module.buffers() if b.is_floating_point()
+                       or b.dtype in (torch.int64, torch.int32)]
+            if self.loopback is not None:
+                self.loopback.broadcast_(f"params", flat)
+                for i, b in enumerate(buffers):
+                    self.loopback.broadcast_(f"buffer{i}", b)
+            elif self.world > 1:
                 torch.distributed.broadcast(flat, src=0, group=self.group)
+                for b in buffers:
+                    if b.device == flat.device:
+                        torch.distributed.broadcast(b, src=0, group=self.group)
             if self.comm.master is not None:
                 self.comm.master.copy_(flat.float())
         torch.cuda.synchronize(self.device)
@@ -218,21 +245,65 @@ class DeftDataParallel:
                         batch_size: int = 1) -> ModelProfile:
         """CUDA-event timing of forward/backward per initial bucket plus the
         measured comm time of every bucket on each channel -> ModelProfile.
-        (B200 replacement of the paper's Nsight profiler.)"""
+        (B200 replacement of the paper's Nsight profiler.)
+        Like the reference's trace reconstruction (trace.py:240-250) every
+        per-bucket time is the median_low over the timed iterations, in integer
+        us.  ``self.profile_step_us`` keeps the median_low end-to-end
+        forward+backward time of the same iterations (the per-bucket times
+        partition it)."""
+        import statistics
         ranges = self.initial_buckets()
+        if self.loopback is not None and self.rank > 0:
+            # loopback: rank 0 measured (all ranks' comm included); same numbers
+            fwd_us, bwd_us, comm_sm, ce_ratio, step_us = self.loopback.broadcast_obj(
+                "profile", None)
+        else:
+            fwd_us, bwd_us, step_us = self._time_buckets(ranges, batch, loss_fn, iters)
+            comm_sm = self._measure_comm(ranges, _native.CHANNEL_SM)
+            ce_ratio = None
+            if self.world > 1 and self.cfg.use_ce_channel:
+                comm_ce = self._measure_comm(ranges, _native.CHANNEL_CE)
+                ratios = sorted(c / s for c, s in zip(comm_ce, comm_sm) if s > 0)
+                ce_ratio = statistics.median_low(ratios) if ratios else None
+            if self.loopback is not None:
+                self.loopback.broadcast_obj("profile",
+                                            (fwd_us, bwd_us, comm_sm, ce_ratio, step_us))
+        if self.world > 1 and self.loopback is None:
+            # every rank must plan the SAME schedule: rank 0's numbers win
+            obj = [(fwd_us, bwd_us, comm_sm, ce_ratio, step_us)]
+            torch.distributed.broadcast_object_list(obj, src=0, group=self.group)
+            fwd_us, bwd_us, comm_sm, ce_ratio, step_us = obj[0]
+        self.profile_step_us = step_us
+        self.comm_us = {"sm": list(comm_sm)}
+        buckets = tuple(
+            BucketProfile(i + 1, hi - lo, fwd_us[i], bwd_us[i], max(1, comm_sm[i]))
+            for i, (lo, hi) in enumerate(ranges))
+        self.cluster = self._make_links(ce_ratio)
+        self.profile = ModelProfile(name=name, buckets=buckets, batch_size=batch_size,
+                                    learning_rate=self.cfg.lr,
+                                    notes={"device": torch.cuda.get_device_name(self.device),
+                                           "world": self.world})
+        return self.profile
+
+    def _time_buckets(self, ranges, batch, loss_fn, iters):
+        """Per-bucket forward / backward us (median_low over `iters` timed
+        iterations after one warm-up) and the end-to-end fwd+bwd us."""
+        import statistics
         owner = self._owner_map(ranges)
-        fwd_ms = [0.0] * len(ranges)
-        bwd_ms = [0.0] * len(ranges)
+        nb = len(ranges)
+        per_f: list[list[int]] = [[] for _ in range(nb)]
+        per_b: list[list[int]] = [[] for _ in range(nb)]
+        per_step: list[int] = []
         module_first = {}
         for m in self.module.modules():
             ps = [p for p in m.parameters(recurse=False) if p.requires_grad]
             if ps:
                 module_first[m] = max(max(owner[id(p)]) for p in ps)
-        for _ in range(iters + 1):
+        for it in range(iters + 1):
             starts: dict[int, torch.cuda.Event] = {}
             hooks = []
 
-            def pre(mod, _inp, b=None):
+            def pre(mod, _inp):
                 b = module_first[mod]
                 if b not in starts:
                     e = torch.cuda.Event(enable_timing=True)
@@ -241,8 +312,7 @@ class DeftDataParallel:
             for m in module_first:
                 hooks.append(m.register_forward_pre_hook(pre))
             done: dict[int, torch.cuda.Event] = {}
-            pending = [len([p for p in self.params if b in owner[id(p)]])
-                       for b in range(len(ranges))]
+            pending = [len([p for p in self.params if b in owner[id(p)]]) for b in range(nb)]
 
             def acc(p):
                 for b in owner[id(p)]:
@@ -267,42 +337,30 @@ class DeftDataParallel:
             for h in hooks:
                 h.remove()
             torch.cuda.synchronize(self.device)
-            if _ == 0:
+            if it == 0:
                 continue  # warm-up
             # forward: bucket n first; bucket b spans start[b] .. start[b-1]
-            nb = len(ranges)
+            us = lambda ms: int(round(ms * 1000.0))  # noqa: E731
             marks = {b: ev0.elapsed_time(starts[b]) for b in starts}
             prev_t = ev0.elapsed_time(ev1)
+            f = [0.0] * nb
             for b in range(nb):  # b = 0 is bucket 1 (output side)
                 t0 = marks.get(b, prev_t)
-                fwd_ms[b] += max(0.0, prev_t - t0) / iters
+                f[b] = max(0.0, prev_t - t0)
                 prev_t = min(prev_t, t0)
-            fwd_ms[nb - 1] += max(0.0, prev_t) / iters  # pre-module prologue -> input bucket
+            f[nb - 1] += max(0.0, prev_t)  # pre-module prologue -> input bucket
             prev_t = ev0.elapsed_time(ev1)
+            t_end = ev0.elapsed_time(ev2)
             for b in range(nb):
-                t1 = ev0.elapsed_time(done[b]) if b in done else ev0.elapsed_time(ev2)
-                bwd_ms[b] += max(0.0, t1 - prev_t) / iters
+                t1 = ev0.elapsed_time(done[b]) if b in done else t_end
+                per_b[b].append(us(max(0.0, t1 - prev_t)))
                 prev_t = max(prev_t, t1)
-        comm_sm = self._measure_comm(ranges, _native.CHANNEL_SM)
-        ce_ratio = None
-        if self.world > 1 and self.cfg.use_ce_channel:
-            comm_ce = self._measure_comm(ranges, _native.CHANNEL_CE)
-            ratios = sorted(c / s for c, s in zip(comm_ce, comm_sm) if s > 0)
-            ce_ratio = ratios[len(ratios) // 2] if ratios else None
-        if self.world > 1:  # every rank must plan the SAME schedule: rank 0's numbers win
-            obj = [(fwd_ms, bwd_ms, comm_sm, ce_ratio)]
-            torch.distributed.broadcast_object_list(obj, src=0, group=self.group)
-            fwd_ms, bwd_ms, comm_sm, ce_ratio = obj[0]
-        buckets = tuple(
-            BucketProfile(i + 1, hi - lo, max(0, round(fwd_ms[i] * 1000)),
-                          max(0, round(bwd_ms[i] * 1000)), max(1, round(comm_sm[i] * 1000)))
-            for i, (lo, hi) in enumerate(ranges))
-        self.cluster = self._make_links(ce_ratio)
-        self.profile = ModelProfile(name=name, buckets=buckets, batch_size=batch_size,
-                                    learning_rate=self.cfg.lr,
-                                    notes={"device": torch.cuda.get_device_name(self.device),
-                                           "world": self.world})
-        return self.profile
+                per_f[b].append(us(f[b]))
+            per_b[nb - 1][-1] += us(max(0.0, t_end - prev_t))   # backward tail -> last bucket
+            per_step.append(us(t_end))
+        med = statistics.median_low
+        return ([max(0, med(x)) for x in per_f], [max(0, med(x)) for x in per_b],
+                med(per_step))
 
     def _owner_map(self, ranges):
         owner = {}
@@ -311,23 +369,40 @@ class DeftDataParallel:
             owner[id(p)] = [b for b, (a, z) in enumerate(ranges) if a < hi and lo < z]
         return owner
 
-    def _measure_comm(self, ranges, channel, reps: int = 3) -> list[float]:
+    def _measure_comm(self, ranges, channel, reps: int = 3) -> list[int]:
+        """Reduce-scatter time (us, median_low of `reps` after one warm-up) of
+        every bucket on one channel.  W = 1: no transfer, 0."""
+        import statistics
         if self.world == 1:
-            return [0.0] * len(ranges)
-        s = torch.cuda.Stream(self.device)
+            return [0] * len(ranges)
+        if self.loopback is not None:
+            # every rank's launch, then one synchronize (rank 0 alone would wait
+            # for its peers forever); the last-launched rank's time is the one
+            # without launch skew
+            ranks = self.loopback.lb.ranks
+            comms = self.loopback.peers()
+            streams = [rk.comm_stream for rk in ranks]
+        else:
+            comms, streams = [self.comm], [torch.cuda.Stream(self.device)]
         out = []
         torch.cuda.synchronize(self.device)
         for lo, hi in ranges:
-            best = float("inf")
-            for _ in range(reps + 1):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(s)
-                self.comm.reduce_scatter(channel, 0, lo, hi - lo, s)
-                b.record(s)
-                b.synchronize()
-                best = min(best, a.elapsed_time(b))
-            out.append(best)
-        self.comm.grads[0].zero_()
+            times = []
+            for rep in range(reps + 1):
+                evs = []
+                for c, s in zip(comms, streams):
+                    a = torch.cuda.Event(enable_timing=True)
+                    b = torch.cuda.Event(enable_timing=True)
+                    a.record(s)
+                    c.reduce_scatter(channel, 0, lo, hi - lo, s)
+                    b.record(s)
+                    evs.append((a, b))
+                torch.cuda.synchronize(self.device)
+                if rep:
+                    times.append(int(round(evs[-1][0].elapsed_time(evs[-1][1]) * 1000.0)))
+            out.append(statistics.median_low(times))
+        for c in comms:
+            c.grads[0].zero_()
         torch.cuda.synchronize(self.device)
         return out
 
@@ -341,6 +416,19 @@ class DeftDataParallel:
         cluster = cluster or self.cluster
         if profile is None or cluster is None:
             raise DeftError("measure_profile() or an explicit profile/cluster is required")
+        if getattr(self, "_planned", False):
+            # re-planning: drop the previous plan's hooks and per-plan caches (a
+            # new schedule starts; groups of the old one still in flight are
+            # dropped, as unaccounted iterations are in the reference)
+            if self._deferred:
+                raise DeftError("plan() again with deferred transfers pending: "
+                                "call finish() first")
+            for h in getattr(self, "_hooks", []):
+                h.remove()
+            self._hooks = []
+        self._groups_cache = None
+        self._fwd_wait = {}
+        self._deferred = []
         if cluster is not self.cluster:
             self.cluster = cluster
             # measured links carry their channel in the name (_make_links); any
@@ -349,6 +437,13 @@ class DeftDataParallel:
                 _native.CHANNEL_CE if l.name == "nvlink_ce" else
                 _native.CHANNEL_SM if l.name == "nvlink_sm" or l.is_fast else
                 _native.CHANNEL_CE for l in cluster.links]
+        if self.world > 1 and len(set(self.channel_of_link)) != len(self.channel_of_link):
+            # one stream, one barrier set and one staging area per channel: two
+            # links on the same channel would interleave their barriers and share
+            # the copy-engine staging buffer
+            raise DeftError(f"links {[l.name for l in cluster.links]} map to channels "
+                            f"{self.channel_of_link}: at most one link per channel "
+                            "(nvlink_sm, nvlink_ce)")
         mult = self.cfg.capacity_multiplier
         self.verdict = None
         if self.cfg.walk is not None and not self.sync:
@@ -396,7 +491,10 @@ class DeftDataParallel:
             (2 if self.placement == "start" else 1)
         self.planner = ExecutionPlanner(self.scheduler, self.cfg.n_slots, self.cfg.lookahead,
                                         lag=lag)
-        self.link_streams = [torch.cuda.Stream(self.device) for _ in cluster.links]
+        if self.loopback is not None:
+            self.link_streams = [self.loopback.comm_stream for _ in cluster.links]
+        else:
+            self.link_streams = [torch.cuda.Stream(self.device) for _ in cluster.links]
         # runtime state
         self._slot_free = [None] * self.cfg.n_slots   # event: slot reusable (async mode)
         self._rs_done: dict[tuple[int, int], torch.cuda.Event] = {}
@@ -425,6 +523,7 @@ class DeftDataParallel:
         self._deferred: list[tuple[int, int, tuple]] = []
         self._defer_tail = (not self.sync and self.world > 1 and self._sequential
                             and self.cfg.defer_tail)
+        self._planned = True
         return part
 
     def decisions(self, t: int) -> tuple[ScheduleDecision, ScheduleDecision]:
@@ -514,11 +613,19 @@ class DeftDataParallel:
     def _install_forward_waits(self):
         """"start" placement: the forward pre-hook of every module that owns
         parameters makes the compute stream wait for the update of the buckets
-        those parameters live in (only the first wait per bucket does anything)."""
+        those parameters live in (only the first wait per bucket does anything).
+        A parameter read without its owning module's forward running (a
+        ParameterList a parent iterates, a weight a parent uses directly) gets
+        no pre-hook: the first forward records which buckets the hooks cover,
+        and the others wait before the forward starts (``_unhooked``)."""
         owner = {id(p): bl for p, bl in zip(self.params, self._param_buckets)}
         self._fwd_wait: dict[int, torch.cuda.Event] = {}
+        self._fwd_seen: set | None = None      # buckets the hooks covered (first forward)
+        self._unhooked: set | None = None      # None = not known yet: wait for all
 
         def pre(mod, _args):
+            if self._fwd_seen is not None:
+                self._fwd_seen.update(self._module_buckets[mod])
             if not self._fwd_wait:
                 return
             stream = torch.cuda.current_stream(self.device)
@@ -695,8 +802,16 @@ class DeftDataParallel:
         ev_fwd = torch.cuda.Event()
         ev_fwd.record(comp)
         self._issue_deferred(ev_fwd)
-        if self.placement == "start" and it.due:
-            self._updates_at_start(comp, it.due)
+        if self.placement == "start":
+            if self._unhooked is None:
+                self._fwd_seen = set()
+            if it.due:
+                self._updates_at_start(comp, it.due)
+                for b in (range(len(self.buckets)) if self._unhooked is None
+                          else self._unhooked):
+                    ev = self._fwd_wait.pop(b, None)    # no pre-hook will wait for it
+                    if ev is not None:
+                        comp.wait_event(ev)
         self._issue_planned(it.fwd, ev_fwd)
         with self._autocast():
             loss = loss_fn(self.module, batch)
@@ -704,6 +819,9 @@ class DeftDataParallel:
             for ev in self._fwd_wait.values():   # buckets no forward module touched
                 comp.wait_event(ev)
             self._fwd_wait = {}
+            if self._fwd_seen is not None:
+                self._unhooked = set(range(len(self.buckets))) - self._fwd_seen
+                self._fwd_seen = None
         if it.zero:
             # store: autograd allocates fresh gradients (no accumulate kernels) and
             # each bucket is gathered into the group slot when its backward ends
@@ -892,18 +1010,35 @@ class DeftDataParallel:
         self.compute_stream.synchronize()
         g = torch.cuda.CUDAGraph()
         n0 = _native.launch_count()
-        with torch.cuda.graph(g, pool=self._pool, stream=self.compute_stream):
-            loss = self._run_iteration(it, static, loss_fn)
+        if self.loopback is not None:
+            # torch.cuda.graph() synchronizes the whole device first, which in a
+            # loopback world would wait for peers whose iteration is not issued
+            with torch.cuda.stream(self.compute_stream):
+                g.capture_begin(pool=self._pool)
+                try:
+                    loss = self._run_iteration(it, static, loss_fn)
+                finally:
+                    g.capture_end()
+        else:
+            with torch.cuda.graph(g, pool=self._pool, stream=self.compute_stream):
+                loss = self._run_iteration(it, static, loss_fn)
         n = _native.launch_count() - n0
         self._captured_native += n
         self._graphs[key] = (g, loss, n, tuple(self._deferred))
-        g.replay()
+        if self.loopback is not None:
+            # graph instantiation synchronizes the device: no rank may replay a
+            # new shape before every rank has captured it (LoopbackWorld.flush)
+            self.loopback.defer_replay(g, self.compute_stream)
+        else:
+            g.replay()
         self._replayed_native += n
         self.last_step_kind = "capture"
         return loss
 
-    def finish(self):
-        """Make theta^(t) current (t = iterations run) and drain every stream.
+    def finish(self, sync: bool = True):
+        """Make theta^(t) current (t = iterations run) and drain every stream
+        (``sync=False``: only issue the work -- a loopback world issues every
+        rank's finish before it synchronizes).
         With "start" placement the updates that become visible at iteration t are
         applied here (they would otherwise run at the start of iteration t); groups
         still in flight stay unapplied, as in the reference where unaccounted
@@ -933,7 +1068,8 @@ class DeftDataParallel:
                         comp.wait_event(ev)
                     self._fwd_wait = {}
                 caller.wait_stream(self.compute_stream)
-        torch.cuda.synchronize(self.device)
+        if sync:
+            torch.cuda.synchronize(self.device)
 
     def timing_summary(self) -> dict:
         """Per-kind (count, total ms, bytes) of the instrumented launches."""

@@ -1,9 +1,16 @@
 import gzip
 import json
+import os
 import sys
 from pathlib import Path
 
 import pytest
+
+# loopback worlds (tests/test_gpu_loopback.py) want one hardware queue per
+# stream; only read when the CUDA context is created
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# ... and no lazily loaded kernel (its first launch waits for the whole device)
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 ROOT = Path(__file__).resolve().parents[1]
 GOLDEN = ROOT / "tests" / "golden"

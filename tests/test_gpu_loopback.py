@@ -1,0 +1,239 @@
+"""Multi-rank parity on ONE GPU (loopback.py): W = 2, 4, 8 ranks in this
+process drive the unchanged reduce-scatter (SM P2P and copy-engine channels),
+fused update + parameter all-gather and barrier kernels, checked against the
+CPU delayed-SGD oracle in the kernels' arithmetic order (fp32 elementwise
+1e-6 relative, bf16 bit for bit), for DeFT and the reference's synchronous
+schedules (scheduler.py:386-418) and every update placement."""
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import smoke_executor as S  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _check(world, iterations, dtype=torch.float32, lag=2, **kw):
+    masters, params, theta0, decisions, buckets, kinds = S.run_loopback(
+        world, iterations, dtype=dtype, **kw)
+    for r in range(1, world):
+        assert decisions[r] == decisions[0], f"rank {r} planned a different stream"
+    want_m, want_p = S.oracle_theta(theta0, decisions[0], world, iterations, dtype=dtype,
+                                    lag=lag)
+    err = S.check_ranks(masters, params, want_m, want_p, world, dtype, buckets)
+    assert not torch.equal(masters[0], theta0), "parameters never moved"
+    return err, decisions[0], kinds
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("placement", ["end", "start", "bucket"])
+@pytest.mark.parametrize("graphs", [True, False])
+def test_loopback_deft_fp32(world, placement, graphs):
+    iters = 14
+    _, decisions, kinds = _check(world, iters, placement=placement, cuda_graphs=graphs)
+    assert max(u["merge_count"] for d in decisions for u in d["update_events"]) >= 2
+    links = {l for d in decisions for p in (d["forward_plan"], d["backward_plan"])
+             for l, ids in p.items() if ids}
+    assert links == {"fast", "twin"}, links    # both channels carried transfers
+    if graphs:
+        assert set(kinds) == {"replay"}, kinds
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("comm_us", [300, 1900])
+def test_loopback_deft_merge_depths(world, comm_us):
+    _check(world, 18, placement="start", cuda_graphs=True, comm_us=comm_us)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("placement", ["end", "start", "bucket"])
+def test_loopback_deft_bf16(world, placement):
+    """bf16 model (the GPT-2 config's bf16 gradient buckets): bf16 slots and
+    parameters, fp32 master (ZeRO-1 style) -- bit for bit with the oracle."""
+    _check(world, 14, dtype=torch.bfloat16, placement=placement,
+           cuda_graphs=placement != "bucket")
+
+
+@pytest.mark.parametrize("scheme", ["wfbp", "priority"])
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("placement", ["end", "start", "bucket"])
+def test_loopback_synchronous_baselines(scheme, world, placement):
+    """Updates of iteration t visible from t+1 (oracle lag 1); priority uses
+    partition_by_size blocks (1000-element buckets cut into 334/333/333)."""
+    iters = 10
+    masters, params, theta0, decisions, buckets, _ = S.run_loopback(
+        world, iters, placement=placement, scheme=scheme,
+        cuda_graphs=placement != "bucket",
+        partition_size=400 if scheme == "priority" else 10**9)
+    d0 = decisions[0]
+    assert all(u["merge_count"] == 1 for d in d0 for u in d["update_events"])
+    want_m, want_p = S.oracle_theta(theta0, d0, world, iters, lag=1)
+    S.check_ranks(masters, params, want_m, want_p, world, torch.float32, buckets)
+    # and it is NOT the delayed trajectory
+    delayed, _ = S.oracle_theta(theta0, d0, world, iters, lag=2)
+    assert S.elem_err(masters[0], delayed) > 1e-4
+
+
+class _ProbeWithUnused(S.Probe):
+    """Parameter 3 never takes part in the loss: its gradient is None."""
+
+    def forward(self, xs):
+        return 0.5 * sum((x * p * p).sum() for i, (p, x) in enumerate(zip(self.ps, xs))
+                         if i != 3)
+
+
+def test_loopback_unused_parameter(monkeypatch):
+    world, iters = 4, 10
+    sizes = S.probe_sizes()
+    order = list(range(len(sizes)))[::-1]
+    offs, o = {}, 0
+    for i in order:
+        offs[i] = (o, o + sizes[i])
+        o += sizes[i]
+    lo, hi = offs[3]
+
+    def x_fn(total, r, t):
+        x = S.flat_x(total, r, t)
+        x[lo:hi] = 0
+        return x
+    masters, params, theta0, decisions, buckets, _ = S.run_loopback(
+        world, iters, model_cls=_ProbeWithUnused, x_fn=S.flat_x, placement="start")
+    want_m, want_p = S.oracle_theta(theta0, decisions[0], world, iters, x_fn=x_fn)
+    S.check_ranks(masters, params, want_m, want_p, world, torch.float32, buckets)
+    assert torch.equal(masters[0][lo:hi], theta0[lo:hi])
+
+
+# ---------------------------------------------------------------------------
+# kernel level: every rank's launch on its own stream, one synchronize
+# ---------------------------------------------------------------------------
+BUCKETS = [(0, 1_000_003), (1_000_003, 7), (1_000_010, 65_536), (1_065_546, 3),
+           (1_065_549, 250_001), (1_315_550, 1), (1_315_551, 200_000)]
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_loopback_reduce_scatter_exact_sum(world, dtype):
+    """Multi-bucket and per-bucket reduce-scatter, SM and copy-engine channels,
+    ragged / tiny / unaligned buckets: shard r of every bucket = the sum over
+    ranks (fp32 accumulation, one rounding to the slot dtype)."""
+    from paper_2503_16815_b200 import _native
+    lbw = S.D.LoopbackWorld(world)
+    total = BUCKETS[-1][0] + BUCKETS[-1][1]
+    comms = lbw.make_comms(2, total, dtype)
+    dev = lbw.device
+    idx = torch.arange(total, device=dev, dtype=torch.float32)
+    mine = [torch.sin(idx * 0.37 + r).to(dtype) for r in range(world)]
+    acc = mine[0].float()
+    for r in range(1, world):
+        acc = acc + mine[r].float()
+    want = acc.to(dtype).float()
+    align = 4 if dtype == torch.float32 else 8
+    for ch in (_native.CHANNEL_SM, _native.CHANNEL_CE):
+        for multi in (True, False):
+            for r in range(world):
+                comms[r].grads[1].copy_(mine[r])
+            torch.cuda.synchronize()
+            for r in range(world):
+                s = lbw.rank(r).comm_stream
+                if multi:
+                    comms[r].reduce_scatter_multi(ch, 1, [(o, o + n) for o, n in BUCKETS], s)
+                else:
+                    for o, n in BUCKETS:
+                        comms[r].reduce_scatter(ch, 1, o, n, s)
+            torch.cuda.synchronize()
+            for r in range(world):
+                got = comms[r].grads[1].float()
+                for o, n in BUCKETS:
+                    lo, hi = S.shard_range(o, n, r, world, align)
+                    if hi > lo:
+                        err = float((got[lo:hi] - want[lo:hi]).abs().max())
+                        # fp32: W-term sums, order may differ (CE: own shard first)
+                        tol = 1e-5 if dtype == torch.float32 else 0.0 if ch == 0 else 0.02
+                        assert err <= tol, (ch, multi, r, o, n, err)
+    for c in comms:
+        c.close()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("blocks", [0, 4])
+def test_loopback_update_allgather(world, dtype, blocks):
+    """Fused update of the owned shards + parameter all-gather (one launch for
+    every bucket of an event): every rank ends with the same parameters, equal
+    to the fma-form SGD step of the reduced gradient."""
+    lbw = S.D.LoopbackWorld(world)
+    total = BUCKETS[-1][0] + BUCKETS[-1][1]
+    comms = lbw.make_comms(2, total, dtype)
+    dev = lbw.device
+    g = torch.Generator(device="cpu").manual_seed(5)
+    p0 = torch.randn(total, generator=g)
+    v0 = torch.randn(total, generator=g)
+    red = torch.randn(total, generator=g).to(dtype)     # the reduced slot (every owner)
+    lr, m, scale = 0.05, 0.9, 1.0 / (world * 3)
+    moms = []
+    for r in range(world):
+        c = comms[r]
+        c.set_update_blocks(blocks)
+        c.params.copy_(p0.to(dtype))
+        if c.master is not None:
+            c.master.copy_(p0.to(dtype).float())
+        c.grads[1].copy_(red)
+        moms.append(v0.to(dev).clone())
+    torch.cuda.synchronize()
+    ranges = [(o, o + n) for o, n in BUCKETS]
+    for r in range(world):
+        comms[r].update_multi(1, ranges, scale, lr, m, moms[r], lbw.rank(r).comm_stream)
+    torch.cuda.synchronize()
+    from oracle.delayed_sgd import _fma32
+    base = p0.to(dtype).float()
+    v = _fma32(torch.tensor(m), v0, red.float() * torch.tensor(scale, dtype=torch.float32))
+    want = _fma32(torch.tensor(-lr), v, base).to(dtype)
+    align = 4 if dtype == torch.float32 else 8
+    for r in range(world):
+        assert torch.equal(comms[r].params.cpu(), want), r
+        vr = moms[r].cpu()
+        for o, n in BUCKETS:
+            lo, hi = S.shard_range(o, n, r, world, align)
+            assert torch.equal(vr[lo:hi], v[lo:hi]), (r, o)
+    for c in comms:
+        c.close()
+
+
+def test_loopback_measure_profile_and_comm():
+    """The B200 profiler in a 4-rank loopback world: per-bucket forward /
+    backward times partition the end-to-end step (within 2 %), and the W > 1
+    transfer time of every bucket and the copy-engine ratio mu are measured."""
+    torch.manual_seed(0)
+    world = 4
+    lbw = S.D.LoopbackWorld(world)
+    execs, models = [], []
+    for r in range(world):
+        torch.manual_seed(0)
+        m = torch.nn.Sequential(*[torch.nn.Sequential(torch.nn.Linear(1024, 1024),
+                                                      torch.nn.ReLU()) for _ in range(8)])
+        m = m.cuda()
+        models.append(m)
+        cfg = S.D.DeftConfig(autocast_dtype=None, cuda_graphs=False,
+                             partition=S.D.PartitionConfig(partition_size=2_200_000))
+        execs.append(S.D.DeftDataParallel(m, cfg, process_group=lbw.rank(r)))
+    x = torch.randn(512, 1024, device=lbw.device)
+
+    def loss_fn(mod, batch):
+        return mod(batch[0]).square().mean()
+    profs = [e.measure_profile((x,), loss_fn, iters=5) for e in execs]
+    p = profs[0]
+    assert all(q == p for q in profs)                 # every rank plans the same profile
+    assert len(p.buckets) >= 3
+    tot = sum(b.forward_us + b.backward_us for b in p.buckets)
+    assert abs(tot - execs[0].profile_step_us) <= 0.02 * execs[0].profile_step_us
+    assert all(b.comm_fast_us > 1 for b in p.buckets)  # measured, not the 1 us floor
+    assert [l.name for l in execs[0].cluster.links] in (["nvlink_sm", "nvlink_ce"],
+                                                       ["nvlink_ce", "nvlink_sm"])
+    assert execs[0].cluster.links[1].speed_ratio_to_fast > 0
+    for e in execs:
+        e.close()
