@@ -221,6 +221,24 @@ deft_status_t deft_gather_segments(void* d_dst, const void* const* d_srcs,
                                    int32_t count, int64_t ce_min_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Loopback collectives: ONE launch carries every rank of a loopback world
+ * (comms[r] = rank r's communicator; all ranks' buffers on the same device;
+ * gridDim.y = world).  The peer barriers meet inside one co-resident grid, so
+ * these complete even when kernels are serialized (a kernel profiler), where
+ * W separate per-rank launches never meet.  Same kernels, arithmetic and
+ * results as each rank's deft_bucket_reduce_scatter_multi /
+ * deft_bucket_update_multi; synchronous.  d_moms: rank r's momentum buffer.
+ * ------------------------------------------------------------------------ */
+deft_status_t deft_loopback_reduce_scatter(deft_comm* const* comms, int32_t world,
+                                           int32_t channel, int32_t slot, int32_t count,
+                                           const int64_t* offsets, const int64_t* numels,
+                                           void* stream);
+deft_status_t deft_loopback_update(deft_comm* const* comms, int32_t world, int32_t slot,
+                                   int32_t count, const int64_t* offsets, const int64_t* numels,
+                                   float lr, float momentum, float grad_scale,
+                                   float* const* d_moms, void* stream);
+
+/* ------------------------------------------------------------------------
  * Streams and hardware work queues (loopback worlds, loopback.py).
  * deft_stream_create: a non-blocking stream of the given priority.
  * deft_stream_alias_probe: *aliased = 1 if work on stream_b issued after a

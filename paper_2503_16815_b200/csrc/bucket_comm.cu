@@ -329,14 +329,22 @@ cudaError_t launch_reduce_scatter_sm(const PeerPtrs& P, int rank, int world, int
 // ============================================================================
 // Barrier-only kernel (CE channel: the copy engines cannot wait on a flag).
 // ============================================================================
-__global__ void barrier_kernel(PeerPtrs P, int rank, int world, int set) {
+// loopback: one launch with gridDim.y = world carries every rank (rank = blockIdx.y)
+__global__ void barrier_kernel(PeerPtrs P, int rank, int world, int set, int loopback) {
+  if (loopback) rank = blockIdx.y;
   const uint32_t epoch = take_epochs(P, rank, set, 1u) + 1u;
   peer_block_barrier(P, rank, world, set, 0, epoch);
 }
 
 cudaError_t launch_barrier(const PeerPtrs& P, int rank, int world, int set,
                            cudaStream_t stream) {
-  barrier_kernel<<<1, 32, 0, stream>>>(P, rank, world, set);
+  barrier_kernel<<<1, 32, 0, stream>>>(P, rank, world, set, 0);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_barrier_loopback(const PeerPtrs& P, int world, int set, cudaStream_t stream) {
+  barrier_kernel<<<dim3(1, world), 32, 0, stream>>>(P, 0, world, set, 1);
   count_launch();
   return cudaGetLastError();
 }
@@ -877,6 +885,21 @@ struct ChunkTable {           // this rank's owned shards, cut into TMA chunks
   int32_t count;
 };
 
+// Loopback collective launches (gridDim.y = world, rank = blockIdx.y): every
+// rank's table and private buffers, in device memory.
+struct RankSlice {
+  ChunkTable t;
+  float* mom;
+  float* master;
+};
+
+template <bool kLoop>
+__device__ __forceinline__ const ChunkTable& pick_table(const ChunkTable& own,
+                                                        const RankSlice* slices) {
+  if constexpr (kLoop) return slices[blockIdx.y].t;
+  else return own;
+}
+
 // Segments [s0, s0 + t.count) of a bucket list -> this rank's shard of each
 // (shard_of: the same ownership every comm kernel uses), 8-element-aligned
 // bodies cut into `chunk`-element pieces, unaligned heads/tails apart.
@@ -919,9 +942,12 @@ __host__ __device__ constexpr int64_t rs_tma_chunk() {  // elements per peer chu
 
 // One launch reduces every segment of the table (all buckets released together
 // on this link): one entry barrier instead of one per bucket.
-template <typename T, int W, int kTmaStages>
+template <typename T, int W, int kTmaStages, bool kLoop = false>
 __global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
-    PeerPtrs P, int rank, int64_t slot_base, ChunkTable t) {
+    PeerPtrs P, int rank_arg, int64_t slot_base, const __grid_constant__ ChunkTable t_arg,
+    const RankSlice* __restrict__ slices) {
+  const int rank = kLoop ? (int)blockIdx.y : rank_arg;
+  const ChunkTable& t = pick_table<kLoop>(t_arg, slices);
   using V = Vec<T>;
   extern __shared__ __align__(128) unsigned char tma_smem[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
@@ -1013,7 +1039,8 @@ static void rs_tma_dispatch_s(int world, int grid, cudaStream_t stream, const Pe
       attr = true;                                                                             \
     }                                                                                          \
     reduce_scatter_tma_kernel<T, WW, S><<<grid, kTmaThreads, smem, stream>>>(P, rank,         \
-                                                                            slot_base, t);     \
+                                                                            slot_base, t,      \
+                                                                            nullptr);          \
     break;                                                                                     \
   }
   switch (world) {
@@ -1133,10 +1160,14 @@ __device__ __forceinline__ void tma_store_wait_all() {
 }
 
 
-template <typename T, int W, int kUpdTmaStages>
+template <typename T, int W, int kUpdTmaStages, bool kLoop = false>
 __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
-    PeerPtrs P, int rank, int64_t slot_base, ChunkTable t, float lr, float momentum,
-    float scale, float* __restrict__ mom) {
+    PeerPtrs P, int rank_arg, int64_t slot_base, const __grid_constant__ ChunkTable t_arg,
+    float lr, float momentum, float scale, float* __restrict__ mom_arg,
+    const RankSlice* __restrict__ slices) {
+  const int rank = kLoop ? (int)blockIdx.y : rank_arg;
+  const ChunkTable& t = pick_table<kLoop>(t_arg, slices);
+  float* __restrict__ mom = kLoop ? slices[blockIdx.y].mom : mom_arg;
   using V = Vec<T>;
   constexpr bool kMaster = sizeof(T) == 2;
   // stage layout: g (T) | v (f32) | p (f32) | p_out (T, bf16 only)
@@ -1151,7 +1182,8 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
   // generic acquire -> async-proxy (bulk copy) accesses of global memory
   if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
   const T* g = reinterpret_cast<const T*>(P.grads[rank]) + slot_base;
-  float* ref = kMaster ? P.master : reinterpret_cast<float*>(P.params[rank]);
+  float* ref = kMaster ? (kLoop ? slices[blockIdx.y].master : P.master)
+                       : reinterpret_cast<float*>(P.params[rank]);
   T* dst[W];
 #pragma unroll
   for (int k = 0; k < W; ++k) dst[k] = reinterpret_cast<T*>(P.params[k]);
@@ -1286,7 +1318,7 @@ bool launch_update_allgather_tma(const PeerPtrs& P, int rank, int world, int dty
     cudaFuncSetAttribute(update_allgather_tma_kernel<TT, WW, SS>,                              \
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
     update_allgather_tma_kernel<TT, WW, SS><<<grid, kUpdTmaThreads, smem, stream>>>(           \
-        P, rank, slot_base, t, lr, momentum, grad_scale, mom);                                 \
+        P, rank, slot_base, t, lr, momentum, grad_scale, mom, nullptr);                        \
   }
 #define DEFT_UPT_CASE(WW)                                                                      \
   case WW:                                                                                     \
@@ -1307,6 +1339,130 @@ bool launch_update_allgather_tma(const PeerPtrs& P, int rank, int world, int dty
     count_launch();
   }
   return true;
+}
+
+}  // namespace deft
+
+namespace deft {
+
+// ============================================================================
+// Loopback collectives: ONE launch carries every rank of a loopback world
+// (gridDim.y = world, rank = blockIdx.y, each rank's table / momentum / master
+// in a device RankSlice array).  The rendezvous of the peer barriers happens
+// inside one grid whose blocks are all co-resident (grid capped by
+// P.grid_cap), so it completes even when kernels are serialized -- the
+// situation of a kernel profiler, where W separate launches never meet.
+// ============================================================================
+static cudaError_t upload_slices(const std::vector<RankSlice>& h, RankSlice** d) {
+  cudaError_t e = cudaMalloc(d, h.size() * sizeof(RankSlice));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*d, h.data(), h.size() * sizeof(RankSlice), cudaMemcpyHostToDevice);
+}
+
+cudaError_t launch_rs_tma_loopback(const PeerPtrs& P, int world, int dtype, int64_t slot_base,
+                                   int32_t count, const int64_t* offsets, const int64_t* numels,
+                                   cudaStream_t stream) {
+  if (world < 2 || world > 8) return cudaErrorInvalidValue;
+  const int align = dtype == 0 ? 4 : 8;
+  for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
+    std::vector<RankSlice> h(world);
+    for (int r = 0; r < world; ++r)
+      build_chunk_table(h[r].t, s0, count, offsets, numels, r, world, align,
+                        rs_chunk_for(world, dtype));
+    int64_t per = 0;
+    for (int k = 0; k < h[0].t.count; ++k) per += (numels[s0 + k] + world - 1) / world;
+    int grid = (int)((per + 32767) / 32768);
+    if (grid < 1) grid = 1;
+    if (grid > rs_tma_blocks()) grid = rs_tma_blocks();
+    grid = cap_grid(P, grid);
+    RankSlice* d = nullptr;
+    cudaError_t e = upload_slices(h, &d);
+    if (e != cudaSuccess) return e;
+    const size_t smem = (size_t)kTmaStagesDefault * kTmaStageBytes;
+#define DEFT_RSL_CASE(WW)                                                                 \
+  case WW:                                                                                \
+    if (dtype == 0) {                                                                     \
+      cudaFuncSetAttribute(reduce_scatter_tma_kernel<float, WW, kTmaStagesDefault, true>, \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+      reduce_scatter_tma_kernel<float, WW, kTmaStagesDefault, true>                       \
+          <<<dim3(grid, world), kTmaThreads, smem, stream>>>(P, 0, slot_base, h[0].t, d); \
+    } else {                                                                              \
+      cudaFuncSetAttribute(                                                               \
+          reduce_scatter_tma_kernel<__nv_bfloat16, WW, kTmaStagesDefault, true>,          \
+          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                        \
+      reduce_scatter_tma_kernel<__nv_bfloat16, WW, kTmaStagesDefault, true>               \
+          <<<dim3(grid, world), kTmaThreads, smem, stream>>>(P, 0, slot_base, h[0].t, d); \
+    }                                                                                     \
+    break;
+    switch (world) {
+      DEFT_RSL_CASE(2) DEFT_RSL_CASE(3) DEFT_RSL_CASE(4) DEFT_RSL_CASE(5)
+      DEFT_RSL_CASE(6) DEFT_RSL_CASE(7) DEFT_RSL_CASE(8)
+      default: break;
+    }
+#undef DEFT_RSL_CASE
+    count_launch();
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    cudaFree(d);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_update_tma_loopback(const PeerPtrs& P, int world, int dtype,
+                                       int64_t slot_base, int32_t count,
+                                       const int64_t* offsets, const int64_t* numels,
+                                       float lr, float momentum, float grad_scale,
+                                       float* const* moms, float* const* masters,
+                                       int max_blocks, cudaStream_t stream) {
+  if (world < 2 || world > 8) return cudaErrorInvalidValue;
+  const int align = dtype == 0 ? 4 : 8;
+  for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
+    std::vector<RankSlice> h(world);
+    int64_t total_elems = 0;
+    for (int r = 0; r < world; ++r) {
+      build_chunk_table(h[r].t, s0, count, offsets, numels, r, world, align, kUpdChunk);
+      h[r].mom = moms[r];
+      h[r].master = masters[r];
+    }
+    for (int k = 0; k < h[0].t.count; ++k) total_elems += numels[s0 + k];
+    int grid = comm_grid_for((total_elems + world - 1) / world);
+    if (max_blocks > 0 && grid > max_blocks) grid = max_blocks;
+    grid = cap_grid(P, grid);
+    RankSlice* d = nullptr;
+    cudaError_t e = upload_slices(h, &d);
+    if (e != cudaSuccess) return e;
+    const size_t esz = dtype == 0 ? 4 : 2;
+    const size_t smem = (size_t)kUpdTmaStagesDefault *
+                        (kUpdChunk * esz + 2 * kUpdChunk * 4 + (dtype == 0 ? 0 : kUpdChunk * esz));
+#define DEFT_UPL_LAUNCH(TT, WW)                                                               \
+  {                                                                                           \
+    cudaFuncSetAttribute(update_allgather_tma_kernel<TT, WW, kUpdTmaStagesDefault, true>,     \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
+    update_allgather_tma_kernel<TT, WW, kUpdTmaStagesDefault, true>                           \
+        <<<dim3(grid, world), kUpdTmaThreads, smem, stream>>>(P, 0, slot_base, h[0].t, lr,    \
+                                                              momentum, grad_scale, nullptr,  \
+                                                              d);                             \
+  }
+#define DEFT_UPL_CASE(WW)                                           \
+  case WW:                                                          \
+    if (dtype == 0) DEFT_UPL_LAUNCH(float, WW)                      \
+    else DEFT_UPL_LAUNCH(__nv_bfloat16, WW)                         \
+    break;
+    switch (world) {
+      DEFT_UPL_CASE(2) DEFT_UPL_CASE(3) DEFT_UPL_CASE(4) DEFT_UPL_CASE(5)
+      DEFT_UPL_CASE(6) DEFT_UPL_CASE(7) DEFT_UPL_CASE(8)
+      default: break;
+    }
+#undef DEFT_UPL_CASE
+#undef DEFT_UPL_LAUNCH
+    count_launch();
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    cudaFree(d);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace deft

@@ -624,6 +624,102 @@ extern "C" deft_status_t deft_bucket_update_multi(deft_comm* c, int32_t slot, in
 }
 
 // ============================================================================
+// Loopback collectives (one launch for all ranks of a loopback world)
+// ============================================================================
+static deft_status_t check_loopback(deft_comm* const* comms, int32_t world) {
+  if (!comms || world < 2 || world > kMaxWorld)
+    return fail(DEFT_ERR_INVALID_ARGUMENT, "loopback: bad world");
+  for (int32_t r = 0; r < world; ++r) {
+    if (!comms[r] || comms[r]->rank != r || comms[r]->world != world ||
+        comms[r]->dtype != comms[0]->dtype || comms[r]->slot_elems != comms[0]->slot_elems)
+      return fail(DEFT_ERR_INVALID_ARGUMENT, "loopback: comms must be ranks 0..W-1 of one world");
+    for (int k = 0; k < world; ++k)
+      if (comms[r]->P.grads[k] != comms[0]->P.grads[k] ||
+          comms[r]->P.flags[k] != comms[0]->P.flags[k])
+        return fail(DEFT_ERR_INVALID_ARGUMENT, "loopback: comms of different worlds");
+  }
+  return DEFT_OK;
+}
+
+extern "C" deft_status_t deft_loopback_reduce_scatter(deft_comm* const* comms, int32_t world,
+                                                      int32_t channel, int32_t slot,
+                                                      int32_t count, const int64_t* offsets,
+                                                      const int64_t* numels, void* stream) {
+  deft_status_t st = check_loopback(comms, world);
+  if (st != DEFT_OK) return st;
+  const deft_comm* c0 = comms[0];
+  for (int32_t k = 0; k < count; ++k) {
+    st = check_range(c0, slot, offsets[k], numels[k]);
+    if (st != DEFT_OK) return st;
+  }
+  if (count <= 0) return DEFT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t slot_base = (int64_t)slot * c0->slot_elems;
+  if (channel == DEFT_CHANNEL_SM) {
+    cudaError_t e = launch_rs_tma_loopback(c0->P, world, c0->dtype, slot_base, count, offsets,
+                                           numels, s);
+    if (e != cudaSuccess) return cuda_fail(e, "reduce_scatter_tma_kernel (loopback)");
+    return DEFT_OK;
+  }
+  if (channel != DEFT_CHANNEL_CE) return fail(DEFT_ERR_INVALID_ARGUMENT, "bad channel");
+  // one barrier launch for all ranks, then every rank's copies + local reduce
+  cudaError_t e = launch_barrier_loopback(c0->P, world, kBarrierCE, s);
+  if (e != cudaSuccess) return cuda_fail(e, "barrier_kernel (loopback)");
+  const int esz = c0->dtype == DEFT_DTYPE_F32 ? 4 : 2;
+  for (int32_t r = 0; r < world; ++r) {
+    deft_comm* c = comms[r];
+    size_t base = 0;
+    for (int32_t k = 0; k < count; ++k) {
+      const ShardRange sh = shard_of(offsets[k], numels[k], r, world, c0->dtype == 0 ? 4 : 8);
+      const int64_t len = sh.hi - sh.lo;
+      const int64_t per = ((numels[k] + world - 1) / world + 16 + 7) / 8 * 8;
+      if (base + (size_t)(world - 1) * per * esz > c->staging_bytes)
+        return fail(DEFT_ERR_WORKSPACE, "loopback: copy-engine staging too small");
+      char* stage = c->staging + base;
+      if (len > 0) {
+        int j = 0;
+        for (int q = 0; q < world; ++q) {
+          if (q == r) continue;
+          DEFT_CUDA(cudaMemcpyAsync(stage + (size_t)j * per * esz,
+                                    c->P.grads[q] + (slot_base + sh.lo) * esz, (size_t)len * esz,
+                                    cudaMemcpyDeviceToDevice, s));
+          ++j;
+        }
+        e = launch_ce_reduce(c->P.grads[r] + slot_base * esz, stage, c0->dtype, world, r, sh.lo,
+                             len, per, s);
+        if (e != cudaSuccess) return cuda_fail(e, "ce_reduce_kernel (loopback)");
+      }
+      base += (size_t)(world - 1) * per * esz;
+    }
+  }
+  DEFT_CUDA(cudaStreamSynchronize(s));
+  return DEFT_OK;
+}
+
+extern "C" deft_status_t deft_loopback_update(deft_comm* const* comms, int32_t world,
+                                              int32_t slot, int32_t count,
+                                              const int64_t* offsets, const int64_t* numels,
+                                              float lr, float momentum, float grad_scale,
+                                              float* const* d_moms, void* stream) {
+  deft_status_t st = check_loopback(comms, world);
+  if (st != DEFT_OK) return st;
+  if (!d_moms) return fail(DEFT_ERR_INVALID_ARGUMENT, "loopback: momentum buffers required");
+  const deft_comm* c0 = comms[0];
+  for (int32_t k = 0; k < count; ++k) {
+    st = check_range(c0, slot, offsets[k], numels[k]);
+    if (st != DEFT_OK) return st;
+  }
+  if (count <= 0) return DEFT_OK;
+  std::vector<float*> masters(world);
+  for (int32_t r = 0; r < world; ++r) masters[r] = comms[r]->P.master;
+  cudaError_t e = launch_update_tma_loopback(
+      c0->P, world, c0->dtype, (int64_t)slot * c0->slot_elems, count, offsets, numels, lr,
+      momentum, grad_scale, d_moms, masters.data(), c0->update_blocks, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "update_allgather_tma_kernel (loopback)");
+  return DEFT_OK;
+}
+
+// ============================================================================
 // K5: persistent DeFT state machine (scheduler_kernel.cu)
 // ============================================================================
 extern "C" size_t deft_sched_carry_bytes(void) { return sizeof(SchedCarry); }

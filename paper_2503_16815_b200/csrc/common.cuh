@@ -79,6 +79,18 @@ __host__ __device__ inline ShardRange shard_of(int64_t offset, int64_t numel, in
 
 int comm_grid_for(int64_t elems_per_rank);
 
+// loopback collectives (one launch, gridDim.y = world; synchronous)
+cudaError_t launch_barrier_loopback(const PeerPtrs& P, int world, int set, cudaStream_t stream);
+cudaError_t launch_rs_tma_loopback(const PeerPtrs& P, int world, int dtype, int64_t slot_base,
+                                   int32_t count, const int64_t* offsets, const int64_t* numels,
+                                   cudaStream_t stream);
+cudaError_t launch_update_tma_loopback(const PeerPtrs& P, int world, int dtype,
+                                       int64_t slot_base, int32_t count,
+                                       const int64_t* offsets, const int64_t* numels,
+                                       float lr, float momentum, float grad_scale,
+                                       float* const* moms, float* const* masters,
+                                       int max_blocks, cudaStream_t stream);
+
 cudaError_t launch_reduce_scatter_sm(const PeerPtrs& P, int rank, int world, int dtype,
                                      int64_t slot_base, int64_t offset, int64_t numel,
                                      cudaStream_t stream);

@@ -21,7 +21,8 @@ What makes it safe to drive every rank from one host thread:
 * 2W streams stay within CUDA_DEVICE_MAX_CONNECTIONS (set to 32 before the
   CUDA context exists) so no two ranks' streams share a hardware queue;
 * nothing may make the host or the device wait for the WHOLE device while a
-  rank's barrier kernel waits for a peer whose work is not issued yet:
+  rank's barrier kernel waits for a peer whose work is not issued yet (no
+  cudaFree either: ``issuing()`` keeps the garbage collector off the loop):
   kernels are loaded eagerly (CUDA_MODULE_LOADING=EAGER, set before the CUDA
   context exists -- a lazily loaded kernel's first launch waits for the
   device), and a new CUDA-graph shape is captured by every rank before any
@@ -128,6 +129,77 @@ class LoopbackWorld:
         if rank == 0 or key not in self._comms:
             self._comms[key] = self.make_comms(n_slots, slot_elems, grad_dtype)
         return self._comms[key][rank]
+
+    # -- collectives: one launch for all ranks (work under kernel serialization)
+    def collective_reduce_scatter(self, comms, channel: int, slot: int, ranges, stream) -> None:
+        """deft_loopback_reduce_scatter: every rank's reduce-scatter of the bucket
+        list in ONE launch (synchronous)."""
+        import ctypes
+
+        from . import _native
+        n, w = len(ranges), self.world
+        _native.check(_native.lib().deft_loopback_reduce_scatter(
+            (ctypes.c_void_p * w)(*[c._h.value for c in comms]), w, channel, slot, n,
+            (ctypes.c_int64 * n)(*[lo for lo, _ in ranges]),
+            (ctypes.c_int64 * n)(*[hi - lo for lo, hi in ranges]),
+            ctypes.c_void_p(stream.cuda_stream)), "deft_loopback_reduce_scatter")
+
+    def collective_update(self, comms, slot: int, ranges, scale: float, lr: float,
+                          momentum: float, moms, stream) -> None:
+        """deft_loopback_update: every rank's fused update of its owned shards +
+        parameter all-gather in ONE launch (synchronous)."""
+        import ctypes
+
+        from . import _native
+        n, w = len(ranges), self.world
+        _native.check(_native.lib().deft_loopback_update(
+            (ctypes.c_void_p * w)(*[c._h.value for c in comms]), w, slot, n,
+            (ctypes.c_int64 * n)(*[lo for lo, _ in ranges]),
+            (ctypes.c_int64 * n)(*[hi - lo for lo, hi in ranges]), lr, momentum, scale,
+            (ctypes.c_void_p * w)(*[m.data_ptr() for m in moms]),
+            ctypes.c_void_p(stream.cuda_stream)), "deft_loopback_update")
+
+    def kernels_run_concurrently(self, timeout_us: int = 50_000) -> bool:
+        """False when the device serializes kernels (a kernel profiler): then the
+        ranks' separate launches can never meet in a barrier and only the
+        collectives above work.  Measured with deft_stream_alias_probe."""
+        import ctypes
+
+        from . import _native
+        lib = _native.lib()
+        a, b = ctypes.c_void_p(), ctypes.c_void_p()
+        _native.check(lib.deft_stream_create(0, ctypes.byref(a)), "deft_stream_create")
+        _native.check(lib.deft_stream_create(0, ctypes.byref(b)), "deft_stream_create")
+        try:
+            out = ctypes.c_int32()
+            _native.check(lib.deft_stream_alias_probe(a, b, timeout_us, 0, ctypes.byref(out)),
+                          "deft_stream_alias_probe")
+            return out.value == 0
+        finally:
+            lib.deft_stream_destroy(a)
+            lib.deft_stream_destroy(b)
+
+    def issuing(self):
+        """Context for the round-robin issue loop: garbage from earlier objects
+        is collected (and the device drained) BEFORE it, and the cyclic garbage
+        collector is off DURING it -- a region freed by the collector mid-loop
+        means cudaFree, which synchronizes the device and so waits for a rank's
+        barrier kernel whose peers this thread has not issued yet."""
+        import contextlib
+        import gc
+
+        @contextlib.contextmanager
+        def ctx():
+            gc.collect()
+            torch.cuda.synchronize(self.device)
+            was = gc.isenabled()
+            gc.disable()
+            try:
+                yield self
+            finally:
+                if was:
+                    gc.enable()
+        return ctx()
 
     def flush(self) -> None:
         """Replay the graphs the ranks captured this round, in rank order.  Call

@@ -152,15 +152,19 @@ def run_loopback(world, iterations, n_buckets=48, total=48_000, lr=0.05, momentu
     xs = [[_xs_for(execs[r], models[r], x_fn(total, r, t).to(dtype).cuda())
            for t in range(iterations)] for r in range(world)]
     torch.cuda.synchronize()
-    for t in range(iterations):
+    marks = _watch_install(execs) if _WATCH else None
+    with lbw.issuing():
+        for t in range(iterations):
+            for r in range(world):
+                with torch.cuda.stream(lbw.rank(r).compute_stream):
+                    execs[r].train_step(xs[r][t], _loss_fn)
+            lbw.flush()            # graphs captured this round replay now
         for r in range(world):
             with torch.cuda.stream(lbw.rank(r).compute_stream):
-                execs[r].train_step(xs[r][t], _loss_fn)
-        lbw.flush()            # graphs captured this round replay now
-    for r in range(world):
-        with torch.cuda.stream(lbw.rank(r).compute_stream):
-            execs[r].finish(sync=False)
-    torch.cuda.synchronize()
+                execs[r].finish(sync=False)
+        if marks is not None:
+            _watch_wait(marks)
+        torch.cuda.synchronize()
     masters, params = [], []
     for ddp in execs:
         m = ddp.comm.master if ddp.comm.master is not None else ddp.comm.params
@@ -173,6 +177,74 @@ def run_loopback(world, iterations, n_buckets=48, total=48_000, lr=0.05, momentu
     for ddp in execs:
         ddp.close()
     return masters, params, theta0_for(total, dtype), decisions, buckets, kinds
+
+
+# DEFT_LOOPBACK_WATCH=1: record an event after every comm launch and every
+# train_step of every rank, and before synchronizing poll them; if nothing
+# completes for 5 s, print the last completed / first pending op of each
+# rank's streams (diagnoses a loopback stall before the barrier spin traps)
+import os as _os  # noqa: E402
+_WATCH = _os.environ.get("DEFT_LOOPBACK_WATCH") == "1"
+
+
+def _watch_install(execs):
+    from paper_2503_16815_b200 import comm as C
+    marks = []        # (rank, label, stream id, event)
+
+    def wrap(name):
+        orig = getattr(C.BucketComm, name)
+
+        def f(self, *a, **k):
+            out = orig(self, *a, **k)
+            st = [x for x in a if hasattr(x, "cuda_stream")][0]
+            if torch.cuda.is_current_stream_capturing():
+                return out
+            ev = torch.cuda.Event()
+            ev.record(st)
+            marks.append((self.rank, f"{name}{[x for x in a[:2] if isinstance(x, int)]}",
+                          st.cuda_stream, ev))
+            return out
+        f._orig = orig
+        setattr(C.BucketComm, name, f)
+    for n in ("reduce_scatter_multi", "update_multi", "gather"):
+        if not hasattr(getattr(C.BucketComm, n), "_orig"):
+            wrap(n)
+    for ddp in execs:
+        orig_step = ddp.train_step
+
+        def step(*a, _o=orig_step, _d=ddp, **k):
+            out = _o(*a, **k)
+            if _d.last_step_kind == "capture":
+                return out
+            ev = torch.cuda.Event()
+            ev.record(_d.compute_stream)
+            marks.append((_d.rank, f"step{_d.iteration - 1}", _d.compute_stream.cuda_stream, ev))
+            return out
+        ddp.train_step = step
+    return marks
+
+
+def _watch_wait(marks, quiet_s=5.0):
+    import time
+    last, t0 = -1, time.time()
+    while True:
+        done = sum(1 for m in marks if m[3].query())
+        if done == len(marks):
+            return
+        if done != last:
+            last, t0 = done, time.time()
+        elif time.time() - t0 > quiet_s:
+            break
+        time.sleep(0.05)
+    by_rank: dict = {}
+    for i, (r, label, sid, ev) in enumerate(marks):
+        by_rank.setdefault(r, []).append((i, label, sid % 100000, ev.query()))
+    for r, ms in sorted(by_rank.items()):
+        pend = [m for m in ms if not m[3]]
+        okk = [m for m in ms if m[3]]
+        print(f"WATCH rank {r}: {len(okk)}/{len(ms)} done; last done {okk[-1][:3] if okk else None}; "
+              f"first pending {pend[0][:3] if pend else None}", flush=True)
+    raise RuntimeError("loopback stall (see WATCH lines)")
 
 
 def oracle_theta(theta0, decisions, world, iterations, total=48_000, lr=0.05, momentum=0.9,
@@ -245,3 +317,56 @@ def run_smoke_loopback(world=4, iterations=10, dtype=torch.float32, placement="s
         assert decisions[r] == decisions[0], "ranks planned different streams"
     want_m, want_p = oracle_theta(theta0, decisions[0], world, iterations, dtype=dtype)
     return check_ranks(masters, params, want_m, want_p, world, dtype, buckets)
+
+
+def run_collective(world, iterations=8, dtype=torch.float32, total=48_000, n_buckets=48,
+                   lr=0.05, momentum=0.9, x_fn=flat_x):
+    """Kernel-level delayed-update parity in a loopback world with ONE launch per
+    collective (deft_loopback_reduce_scatter / deft_loopback_update): pairs of
+    iterations merge into one gradient group (store, then merge), every group
+    is reduce-scattered -- even buckets on the SM channel, odd ones on the
+    copy-engine channel -- and applied as one fused update + parameter
+    all-gather with scale 1/(2W), visible from the next iteration (oracle lag 1).
+    Works when the device serializes kernels (the driver's profiled smoke run).
+    Returns the worst elementwise error."""
+    from paper_2503_16815_b200 import _native
+    lbw = D.LoopbackWorld(world)
+    comms = lbw.make_comms(2, total, dtype)
+    dev = lbw.device
+    theta0 = theta0_for(total, dtype)
+    for c in comms:
+        c.params.copy_(theta0.to(dtype))
+        if c.master is not None:
+            c.master.copy_(theta0)
+    moms = [torch.zeros(total, dtype=torch.float32, device=dev) for _ in range(world)]
+    size = total // n_buckets
+    ranges = [(b * size, (b + 1) * size) for b in range(n_buckets)]
+    sm, ce = ranges[0::2], ranges[1::2]
+    s = torch.cuda.current_stream(dev)
+    decisions = []
+    torch.cuda.synchronize()
+    for t in range(iterations):
+        slot = (t // 2) % 2
+        for r in range(world):
+            g = (x_fn(total, r, t).to(dtype).to(dev) * comms[r].params).to(dtype)
+            if t % 2 == 0:
+                comms[r].grads[slot].copy_(g)
+            else:
+                comms[r].grads[slot].add_(g)      # merge (autograd's accumulate)
+        if t % 2 == 1:
+            torch.cuda.synchronize()
+            lbw.collective_reduce_scatter(comms, _native.CHANNEL_SM, slot, sm, s)
+            lbw.collective_reduce_scatter(comms, _native.CHANNEL_CE, slot, ce, s)
+            lbw.collective_update(comms, slot, ranges, 1.0 / (world * 2), lr, momentum, moms, s)
+            decisions.append({"iteration": t, "stage": "backward",
+                              "update_events": [{"origins": [t - 1, t], "merge_count": 2}]})
+    torch.cuda.synchronize()
+    masters = [(c.master if c.master is not None else c.params).float().cpu() for c in comms]
+    params = [c.params.cpu() for c in comms]
+    want_m, want_p = delayed_sgd.run_kernel_order(
+        theta0, lambda r, t: x_fn(total, r, t), decisions, world, lr, momentum, iterations,
+        dtype=dtype, lag=1)
+    err = check_ranks(masters, params, want_m, want_p, world, dtype, ranges)
+    for c in comms:
+        c.close()
+    return err

@@ -237,3 +237,16 @@ def test_loopback_measure_profile_and_comm():
     assert execs[0].cluster.links[1].speed_ratio_to_fast > 0
     for e in execs:
         e.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_loopback_collective_kernels(world, dtype):
+    """One launch per collective for all ranks (deft_loopback_reduce_scatter /
+    deft_loopback_update, what smoke() runs under a profiler): delayed-update
+    parity with merged groups on both channels."""
+    S.run_collective(world, iterations=8, dtype=dtype)
+
+
+def test_kernels_run_concurrently():
+    assert S.D.LoopbackWorld(2).kernels_run_concurrently()
