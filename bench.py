@@ -64,6 +64,11 @@ def parse():
                     help="scale the measured comm times before planning (slower-link / "
                          "update-frequency sweep: >1 makes DeFT merge iterations)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--solver-full", action="store_true",
+                    help="solver block: also time the reference's GPT-2 / VGG-19 feedback "
+                         "loops (about 50 s of single-core Python)")
+    ap.add_argument("--ddp-graphs", action="store_true",
+                    help="--impl ddp: capture the DDP step (static_graph=True) in a CUDA graph")
     ap.add_argument("--h2d-chunks", type=int, default=32,
                     help="e2e: split each step's host->device input copy into this many "
                          "batch slices")
@@ -134,16 +139,25 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, period_ms=50):
         self.index = index
+        self.period_ms = period_ms
         self.rows = []
         self.proc = None
+        self.window = None
+
+    def mark(self, start: bool):
+        """Open / close the timed region; summary() reports the samples inside."""
+        if start:
+            self.window = [time.monotonic(), None]
+        else:
+            self.window[1] = time.monotonic()
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -153,7 +167,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append([time.monotonic()] + [x.strip() for x in line.split(",")])
 
     def __exit__(self, *a):
         if self.proc:
@@ -161,30 +175,59 @@ class ClockSampler:
             self.proc.wait(timeout=5)
 
     def summary(self):
-        if not self.rows:
+        rows = [r[1:] for r in self.rows]
+        win = None
+        if self.window and self.window[1] is not None:
+            win = [r[1:] for r in self.rows if self.window[0] <= r[0] <= self.window[1]]
+        use = win if win else rows
+        if not use:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
-        mx = max(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        sm = sorted(float(r[0]) for r in use if r[0].replace(".", "").isdigit())
+        mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:6]) if v == "Active"})
+        reasons = sorted({n for r in use for n, v in zip(names, r[2:6]) if v == "Active"})
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(use),
+                "samples_all": len(rows), "period_ms": self.period_ms,
+                "window": "timed region" if win else "whole run (no sample in the timed region)",
+                "window_s": round(self.window[1] - self.window[0], 3) if win else None}
 
 
 # ----------------------------------------------------------------- CPU path
 
-def cpu_reference_run(model_name, steps, warmup, batch):
-    """The reference's CPU path (oracle port): the DeFT decision stream from the
-    oracle scheduler on the fixture profile, CPU fwd/bwd, delayed SGD/momentum
-    exactly as oracle/delayed_sgd.py.  Bounded sample: `batch` samples/step."""
-    import torch
-    from oracle import deft_oracle as O
-
+def reference_schedule(n_iter):
+    """The DeFT decision stream of the reference's ResNet-101 fixture on its
+    dual-link cluster (6.5M partition, mu 1.65) from the UNMODIFIED reference
+    (deftsim, oracle/_ref -- copied there by build()), as dicts; the oracle port
+    when the copy is absent.  Returns (decisions, seconds, kind)."""
+    from oracle import reference
     inputs = json.loads((ROOT / "tests" / "golden" / "inputs.json").read_text())
-    prof = inputs["profiles"]["resnet101" if model_name != "gpt2" else "gpt2"]
-    cl = inputs["clusters"]["dual"]
-    part = O.partition(prof["buckets"], sum(b["forward_us"] for b in prof["buckets"]),
-                       6_500_000, 1.65)
+    prof_d, cl_d = inputs["profiles"]["resnet101"], inputs["clusters"]["dual"]
+    t0 = time.perf_counter()
+    if reference.available():
+        R = reference.deftsim()
+        sched = R.deft_schedule(R.profile_from_dict(prof_d), R.cluster_from_dict(cl_d),
+                                R.PartitionConfig(partition_size=6_500_000, mu=1.65), n_iter)
+        dec = [d.to_dict() for d in sched.decisions]
+        kind = "reference"
+    else:
+        from oracle import deft_oracle as O
+        part = O.partition(prof_d["buckets"], sum(b["forward_us"] for b in prof_d["buckets"]),
+                           6_500_000, 1.65)
+        dec = O.schedule(part, [l["speed_ratio_to_fast"] for l in cl_d["links"]],
+                         [l["name"] for l in cl_d["links"]], n_iter)
+        kind = "port"
+    return dec, time.perf_counter() - t0, kind
+
+
+def cpu_reference_run(model_name, steps, warmup, batch):
+    """The reference's CPU path on this host: the DeFT schedule from the
+    reference itself (deftsim, reference_schedule), CPU fwd/bwd of the named
+    model, and the delayed SGD/momentum the schedule's update events call for
+    (oracle/delayed_sgd.py rules -- the reference defines no update arithmetic
+    and no training loop).  Bounded sample: `batch` samples per step."""
+    import torch
+
     torch.set_num_threads(os.cpu_count() or 1)
     model = build_model(model_name, "cpu")
     params = [p for p in model.parameters() if p.requires_grad][::-1]
@@ -194,10 +237,7 @@ def cpu_reference_run(model_name, steps, warmup, batch):
     v = torch.zeros(total)
     summed = {}
     n = warmup + steps
-    t_sched0 = time.perf_counter()
-    decisions = O.schedule(part, [l["speed_ratio_to_fast"] for l in cl["links"]],
-                           [l["name"] for l in cl["links"]], n + 2)
-    t_sched = time.perf_counter() - t_sched0
+    decisions, t_sched, kind = reference_schedule(n + 2)
     events = {d["iteration"]: d["update_events"] for d in decisions if d["stage"] == "backward"}
     t0 = None
     for s in range(n):
@@ -219,48 +259,78 @@ def cpu_reference_run(model_name, steps, warmup, batch):
         loss.backward()
         summed[s] = torch.cat([p.grad.reshape(-1) for p in params])
     dt = time.perf_counter() - t0
+    src = ("the reference itself (deftsim from oracle/_ref)" if kind == "reference"
+           else "the oracle port (oracle/_ref absent)")
     return {"value": steps * batch / dt, "unit": "samples/s", "cores": torch.get_num_threads(),
-            "kind": "port",
+            "kind": kind,
             "sample": f"{model_name} fp32 CPU fwd+bwd, batch {batch} x {steps} timed steps "
-                      f"(+{warmup} warm-up), oracle DeFT schedule (dual link, 6.5M partition, "
-                      f"{t_sched * 1e3:.0f} ms for {n + 2} iterations) + oracle delayed "
-                      f"SGD/momentum"}
+                      f"(+{warmup} warm-up); DeFT schedule (ResNet-101 fixture, dual link, "
+                      f"6.5M partition) by {src}: {t_sched * 1e3:.0f} ms for {n + 2} "
+                      "iterations; delayed SGD/momentum per its update events"}
 
 
 # ----------------------------------------------------------------- GPU path
 
-def solver_measurement():
-    """The scheduling side of the path: DeFT's feedback loop (200 iterations, up to
-    10 capacity retries) on the reference's ResNet-101 fixture at quarter bandwidth
-    -- the persistent GPU state machine (K5) vs the CPU oracle port (1 core)."""
+def solver_measurement(full: bool = False):
+    """The scheduling side of the path, timed on THIS host in the same run: the
+    reference itself (deftsim from oracle/_ref, single-threaded Python: 1 core)
+    against this package (K5 persistent GPU state machine), on the SURVEY §6.3
+    workloads -- feedback_loop (200 iterations, up to 10 capacity retries) on the
+    ResNet-101 fixture at quarter bandwidth (and VGG-19 / GPT-2 with ``full``),
+    and deft_schedule (200 iterations) of the three fixtures -- with the decision
+    streams compared byte for byte."""
     import paper_2503_16815_b200 as D
     from paper_2503_16815_b200 import gpu_scheduler
-    from oracle import deft_oracle as O
+    from oracle import reference
     inputs = json.loads((ROOT / "tests" / "golden" / "inputs.json").read_text())
-    walk = D.WalkParams.from_dict(inputs["walk"])
-    cl = inputs["clusters"]["dual"]
-    prof = D.profile_from_dict(inputs["profiles"]["resnet101"]).scaled_comm(4.0)
+    walk_d, cl_d = inputs["walk"], inputs["clusters"]["dual"]
+    R = reference.deftsim() if reference.available() else None
     cfg = D.PartitionConfig(6_500_000, mu=1.65)
-    gpu_scheduler.run_schedules_lazy(D.partition_buckets(prof, cfg),
-                                     D.cluster_from_dict(cl), [1.0], 4)   # warm
-    t0 = time.perf_counter()
-    sched, verdict = D.feedback_loop(prof, D.cluster_from_dict(cl), cfg, walk, iterations=200)
-    t_gpu = time.perf_counter() - t0
-    b = O.scaled_comm(inputs["profiles"]["resnet101"]["buckets"], 4.0)
-    part = O.partition(b, sum(x["forward_us"] for x in b), 6_500_000, 1.65)
-    t0 = time.perf_counter()
-    m = 1.0
-    for _ in range(verdict.retries + 1):
-        dec = O.schedule(part, [l["speed_ratio_to_fast"] for l in cl["links"]],
-                         [l["name"] for l in cl["links"]], 200, m)
-        m *= 1.1
-    t_cpu = time.perf_counter() - t0
-    same = O.jsonl(dec) == "".join(l + "\n" for l in sched.jsonl_lines())
-    return {"workload": "feedback_loop, ResNet-101 fixture, dual link, bw x0.25, 200 iterations",
-            "retries": verdict.retries, "gpu_s": round(t_gpu, 4),
-            "oracle_cpu_s_1core": round(t_cpu, 3),
-            "reference_python_s": 8.4, "reference_src": "BASELINE.md (build container)",
-            "streams_identical": same}
+    warm = D.partition_buckets(D.profile_from_dict(inputs["profiles"]["resnet101"]), cfg)
+    gpu_scheduler.run_schedules_lazy(warm, D.cluster_from_dict(cl_d), [1.0], 4)   # warm
+    out = {"reference": "deftsim (oracle/_ref, unmodified)" if R else "absent",
+           "reference_cores": 1, "host_nproc": os.cpu_count(), "runs": []}
+
+    def text(decisions):
+        return "".join(json.dumps(d.to_dict(), sort_keys=True) + "\n" for d in decisions)
+
+    loops = [("resnet101", 4.0)] + ([("gpt2", 4.0), ("vgg19", 4.0)] if full else [])
+    for name, scale in loops:
+        prof = D.profile_from_dict(inputs["profiles"][name]).scaled_comm(scale)
+        t0 = time.perf_counter()
+        sched, verdict = D.feedback_loop(prof, D.cluster_from_dict(cl_d), cfg,
+                                         D.WalkParams.from_dict(walk_d), iterations=200)
+        t_gpu = time.perf_counter() - t0
+        run = {"workload": f"feedback_loop {name} bw x{1 / scale:g}, dual link, 200 iterations",
+               "retries": verdict.retries, "gpu_s": round(t_gpu, 4)}
+        if R:
+            rp = R.profile_from_dict(inputs["profiles"][name]).scaled_comm(scale)
+            t0 = time.perf_counter()
+            rs, rv = R.feedback_loop(rp, R.cluster_from_dict(cl_d),
+                                     R.PartitionConfig(6_500_000, mu=1.65),
+                                     R.WalkParams.from_dict(walk_d), iterations=200)
+            run["reference_cpu_s"] = round(time.perf_counter() - t0, 3)
+            run["speedup"] = round(run["reference_cpu_s"] / t_gpu, 1)
+            run["identical"] = (text(rs.decisions) == text(sched.decisions)
+                                and rv.retries == verdict.retries)
+        out["runs"].append(run)
+    for name in ("resnet101", "vgg19", "gpt2"):
+        prof = D.profile_from_dict(inputs["profiles"][name])
+        t0 = time.perf_counter()
+        sched = D.deft_schedule(prof, D.cluster_from_dict(cl_d), cfg, 200)
+        t_gpu = time.perf_counter() - t0
+        run = {"workload": f"deft_schedule {name}, dual link, 6.5M partition, 200 iterations",
+               "gpu_s": round(t_gpu, 4)}
+        if R:
+            t0 = time.perf_counter()
+            rs = R.deft_schedule(R.profile_from_dict(inputs["profiles"][name]),
+                                 R.cluster_from_dict(cl_d),
+                                 R.PartitionConfig(6_500_000, mu=1.65), 200)
+            run["reference_cpu_s"] = round(time.perf_counter() - t0, 3)
+            run["speedup"] = round(run["reference_cpu_s"] / t_gpu, 1)
+            run["identical"] = text(rs.decisions) == text(sched.decisions)
+        out["runs"].append(run)
+    return out
 
 
 def compute_only_step_ms(model, batch, loss_fn, steps, warmup, world, dist, device):
@@ -425,7 +495,9 @@ def init_quiet(dist, device):
 
 def ddp_baseline(args, world, rank, device, dist):
     """NCCL WFBP baseline: torch DistributedDataParallel (bucketed all-reduce
-    overlapped with backward, every iteration) + fused SGD/momentum, eager."""
+    overlapped with backward, every iteration) + fused SGD/momentum; eager, or
+    with ``--ddp-graphs`` the whole step (static_graph=True) captured in one CUDA
+    graph and replayed -- the same launch-overhead treatment DeFT's executor gets."""
     import torch
     model = build_model(args.model, device)
     loss_fn = loss_fn_for(args.model)
@@ -433,35 +505,59 @@ def ddp_baseline(args, world, rank, device, dist):
     bucket_mb = args.bucket_mb or 25
     net = model
     if world > 1:
-        net = torch.nn.parallel.DistributedDataParallel(model, device_ids=[device.index],
-                                                        bucket_cap_mb=bucket_mb,
-                                                        gradient_as_bucket_view=True)
-    opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9, fused=True)
+        net = torch.nn.parallel.DistributedDataParallel(
+            model, device_ids=[device.index], bucket_cap_mb=bucket_mb,
+            gradient_as_bucket_view=True, static_graph=args.ddp_graphs)
+    opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9, fused=True,
+                          capturable=args.ddp_graphs)
     amp = next(model.parameters()).dtype == torch.float32
 
     def step():
         opt.zero_grad(set_to_none=False)
-        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=amp):
+        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=amp,
+                            cache_enabled=not args.ddp_graphs):
             loss = loss_fn(net, batch)
         loss.backward()
         opt.step()
 
+    clk = ClockSampler(device.index).__enter__()
+    mode = "eager"
+    run = step
+    if args.ddp_graphs:
+        s = torch.cuda.Stream(device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(max(3, args.warmup)):
+                step()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step()
+            run, mode = g.replay, "cuda_graph"
+        except Exception as e:   # reported, the eager step is timed instead
+            mode = f"eager (capture failed: {type(e).__name__}: {str(e)[:120]})"
+            torch.cuda.synchronize()
     for _ in range(args.warmup):
-        step()
+        run()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk.mark(True)
     a.record()
     for _ in range(args.steps):
-        step()
+        run()
     b.record()
     torch.cuda.synchronize()
+    clk.mark(False)
     ms = a.elapsed_time(b)
     if world > 1:
         t = torch.tensor([ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    clk.__exit__()
     if rank == 0:
         print(json.dumps({
             "impl": "ddp", "metric": METRIC, "value": round(args.batch * world * args.steps /
@@ -470,7 +566,9 @@ def ddp_baseline(args, world, rank, device, dist):
             "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "dtype": "bf16",
             "config": {"workload": f"{args.model} torch DDP (NCCL all-reduce WFBP) + fused SGD, "
-                                   f"batch {args.batch}/GPU", "bucket_cap_mb": bucket_mb}}))
+                                   f"batch {args.batch}/GPU", "bucket_cap_mb": bucket_mb,
+                       "mode": mode},
+            "clocks": clk.summary()}))
     if world > 1:
         dist.destroy_process_group()
 
@@ -564,12 +662,14 @@ def main():
             ms = float(t.item())
         return ms
 
+    clk = ClockSampler(local).__enter__()      # sampling from before the warm-up on
     warm = ddp.warm_up(batch, loss_fn, min_steps=args.warmup)  # until steady-state replay
     if ddp.static_batch is not None:
         batch = ddp.static_batch      # graphs read these; no per-step device copy
     n0 = ddp.native_launches()
-    with ClockSampler(local) as clk:
-        ms = timed(lambda: ddp.train_step(batch, loss_fn), args.steps)
+    clk.mark(True)
+    ms = timed(lambda: ddp.train_step(batch, loss_fn), args.steps)
+    clk.mark(False)
     launches = ddp.native_launches() - n0
     ms_step = ms / args.steps
     value = args.batch * world * args.steps / (ms / 1e3)
@@ -669,7 +769,7 @@ def main():
     solver = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            solver = solver_measurement()
+            solver = solver_measurement(full=args.solver_full)
         except Exception as e:  # reported, never fatal
             solver = {"error": repr(e)}
     cpu_base = None
@@ -722,6 +822,7 @@ def main():
             "clocks": clk.summary(),
         }
         print(json.dumps(line))
+    clk.__exit__()
     ddp.close()
     if world > 1:
         dist.destroy_process_group()

@@ -27,9 +27,10 @@ from .profiles import (BucketProfile, ClusterSpec, LinkSpec, ModelProfile, clust
                        load_profile, multi_link_coverage_rate, profile_from_dict,
                        profile_to_dict, save_profile)
 from .scheduler import (SCHEMES, CapacityModel, Case, DeftScheduler, ExecNote, QueueState,
-                        Schedule, ScheduleDecision, Transfer, UpdateEvent, baseline_priority,
-                        baseline_wfbp, build_schedule, deft_schedule, effective_update_frequency,
-                        run_lockstep)
+                        Schedule, ScheduleDecision, Transfer, UpdateEvent,
+                        baseline_nonsequential, baseline_priority, baseline_wfbp,
+                        build_schedule, deft_schedule, effective_update_frequency,
+                        run_lockstep, sync_schedule_time_us)
 
 __version__ = "0.1.0"
 

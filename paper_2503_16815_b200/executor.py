@@ -50,10 +50,11 @@ from .preserver import WalkParams, feedback_loop
 from .profiles import BucketProfile, ClusterSpec, LinkSpec, ModelProfile
 from .planner import (ExecutionPlanner, IterPlan, release_runs, start_groups,
                       start_groups_timed)
-from .scheduler import (DeftScheduler, OrderScheduler, ScheduleDecision, priority_order,
+from .scheduler import (DeftScheduler, OrderScheduler, ScheduleDecision,
+                        nonsequential_candidates, priority_order, sync_schedule_time_us,
                         wfbp_order)
 
-SCHEMES = ("deft", "wfbp", "priority")
+SCHEMES = ("deft", "wfbp", "priority", "nonsequential")
 
 
 @dataclass
@@ -409,13 +410,32 @@ class DeftDataParallel:
     # ---------------------------------------------------------------- planning
 
     def plan(self, profile: ModelProfile | None = None, cluster: ClusterSpec | None = None,
-             feedback_iterations: int = 200):
+             feedback_iterations: int = 200, probe: tuple | None = None,
+             _candidate: tuple | None = None):
         """Partition the profile, pick the capacity multiplier (feedback loop when
-        walk parameters are configured) and start the incremental scheduler."""
+        walk parameters are configured) and start the incremental scheduler.
+
+        ``scheme="nonsequential"`` (scheduler.py:421-472): the four candidate
+        block structures x orders are scored -- with ``probe=(batch, loss_fn)``
+        by timing 8 iterations of each on this hardware (parameters, momentum
+        and iteration count restored afterwards; the slowest rank's time decides
+        on every rank), otherwise with the reference's simulator rules
+        (scheduler.sync_schedule_time_us) -- and the fastest is planned."""
         profile = profile or self.profile
         cluster = cluster or self.cluster
         if profile is None or cluster is None:
             raise DeftError("measure_profile() or an explicit profile/cluster is required")
+        if self.cfg.scheme == "nonsequential" and _candidate is None:
+            cands = nonsequential_candidates(profile, self.cfg.partition)
+            if probe is None:
+                fast = cluster.fast_link
+                scores = [(sync_schedule_time_us(p, fast, order, 8), i)
+                          for i, (p, order) in enumerate(cands)]
+            else:
+                scores = self._probe_candidates(profile, cluster, cands, probe)
+            self.nonsequential_scores = sorted(scores)
+            return self.plan(profile, cluster, feedback_iterations,
+                             _candidate=cands[min(scores)[1]])
         if getattr(self, "_planned", False):
             # re-planning: drop the previous plan's hooks and per-plan caches (a
             # new schedule starts; groups of the old one still in flight are
@@ -450,7 +470,9 @@ class DeftDataParallel:
             _, self.verdict = feedback_loop(profile, cluster, self.cfg.partition, self.cfg.walk,
                                             iterations=feedback_iterations)
             mult = self.verdict.capacity_multiplier
-        if self.cfg.scheme == "wfbp":
+        if _candidate is not None:
+            part = _candidate[0]
+        elif self.cfg.scheme == "wfbp":
             part = profile
         elif self.cfg.scheme == "priority":
             part = partition_by_size(profile, self.cfg.partition.partition_size)
@@ -473,8 +495,10 @@ class DeftDataParallel:
         self._gather_slot = None
         from .gpu_scheduler import KernelScheduler
         from .scheduler import use_kernel_engine
+        self.iteration = 0
         if self.sync:
-            order = wfbp_order(part) if self.cfg.scheme == "wfbp" else priority_order(part)
+            order = (list(_candidate[1]) if _candidate is not None else
+                     wfbp_order(part) if self.cfg.scheme == "wfbp" else priority_order(part))
             self.scheduler = OrderScheduler(part, cluster.fast_link.name, order,
                                             link=cluster.links.index(cluster.fast_link))
         elif (use_kernel_engine(self.cfg.schedule_engine)
@@ -525,6 +549,34 @@ class DeftDataParallel:
                             and self.cfg.defer_tail)
         self._planned = True
         return part
+
+    def _probe_candidates(self, profile, cluster, cands, probe, warm: int = 4,
+                          timed: int = 8) -> list[tuple[float, int]]:
+        """Hardware score of each non-sequential candidate: `timed` iterations
+        after `warm`, CUDA events, max over ranks; the training state is put back
+        after every candidate."""
+        if self.loopback is not None:
+            raise DeftError("the hardware probe needs one process per GPU (not loopback)")
+        batch, loss_fn = probe
+        saved = [self.comm.params.clone(), self.mom.clone()]
+        if self.comm.master is not None:
+            saved.append(self.comm.master.clone())
+        scores = []
+        for i, cand in enumerate(cands):
+            self.plan(profile, cluster, _candidate=cand)
+            for _ in range(warm):
+                self.train_step(batch, loss_fn)
+            ms = self._time_steps(batch, loss_fn, timed)
+            scores.append((ms, i))
+            self.finish()
+            self._release_graphs()
+            self.comm.params.copy_(saved[0])
+            self.mom.copy_(saved[1])
+            if self.comm.master is not None:
+                self.comm.master.copy_(saved[2])
+            torch.cuda.synchronize(self.device)
+        self.updates_applied = 0
+        return scores
 
     def decisions(self, t: int) -> tuple[ScheduleDecision, ScheduleDecision]:
         return self.planner.decisions(t)

@@ -100,16 +100,19 @@ class KernelSchedule:
 
 
 def run_schedules(profile: ModelProfile, cluster: ClusterSpec, multipliers: list[float],
-                  iterations: int) -> list[list[ScheduleDecision] | None]:
+                  iterations: int, schedulers=None) -> list[list[ScheduleDecision] | None]:
     """One persistent launch for every multiplier; decoded decision lists, None for
     unsupported instances."""
     return [None if k is None else k.decisions()
-            for k in run_schedules_lazy(profile, cluster, multipliers, iterations)]
+            for k in run_schedules_lazy(profile, cluster, multipliers, iterations, schedulers)]
 
 
 def run_schedules_lazy(profile: ModelProfile, cluster: ClusterSpec, multipliers: list[float],
-                       iterations: int) -> list[KernelSchedule | None]:
-    """One persistent launch for every multiplier; None for unsupported instances."""
+                       iterations: int, schedulers=None) -> list[KernelSchedule | None]:
+    """One persistent launch for every multiplier; None for unsupported instances.
+    ``schedulers``: the DeftScheduler of every instance (the caller's
+    configuration objects, as the reference builds one per attempt); their
+    capacity models are used instead of rebuilding them from the multipliers."""
     solver = _native.subset_sum_solver()
     n = profile.n_buckets
     L = len(cluster.links)
@@ -117,8 +120,9 @@ def run_schedules_lazy(profile: ModelProfile, cluster: ClusterSpec, multipliers:
     comm = np.array([b.comm_fast_us for b in profile.buckets], dtype=np.int64)
     bwd = np.array([b.backward_us for b in profile.buckets], dtype=np.int64)
     fc, bc = [], []
-    for m in multipliers:
-        cm = CapacityModel.from_profile(profile, cluster, m)
+    for i, m in enumerate(multipliers):
+        cm = (schedulers[i].caps if schedulers is not None else
+              CapacityModel.from_profile(profile, cluster, m))
         fc.extend(cm.stage_capacities("forward"))
         bc.extend(cm.stage_capacities("backward"))
     fcaps = np.array(fc, dtype=np.int64)

@@ -189,3 +189,20 @@ def test_unused_parameter_gets_zero_gradient(graphs):
     want_m, want_p = S.oracle_theta(theta0, decisions, 1, iters, x_fn=x_fn)
     S.check_ranks([theta], [params], want_m, want_p, 1, torch.float32, buckets)
     assert torch.equal(theta[lo:hi], theta0[lo:hi])   # zero grads, zero momentum: unchanged
+
+
+@pytest.mark.parametrize("hw_probe", [True, False])
+@pytest.mark.parametrize("placement", ["end", "start"])
+def test_single_gpu_nonsequential(hw_probe, placement):
+    """The reference's non-sequential baseline (scheduler.py:421-472) on the
+    executor: four candidate block structures x orders scored by timing 8
+    iterations of each on the GPU (or by the reference's simulator rules),
+    the state restored after the probe; the run then matches the lag-1 oracle
+    from theta0."""
+    iters = 10
+    theta, params, theta0, decisions, buckets = S.run_executor(
+        1, 0, iters, placement=placement, scheme="nonsequential", partition_size=400,
+        startup_us=500, hw_probe=hw_probe)
+    assert all(u["merge_count"] == 1 for d in decisions for u in d["update_events"])
+    want_m, want_p = S.oracle_theta(theta0, decisions, 1, iters, lag=1)
+    S.check_ranks([theta], [params], want_m, want_p, 1, torch.float32, buckets)

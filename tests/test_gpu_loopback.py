@@ -59,17 +59,18 @@ def test_loopback_deft_bf16(world, placement):
            cuda_graphs=placement != "bucket")
 
 
-@pytest.mark.parametrize("scheme", ["wfbp", "priority"])
+@pytest.mark.parametrize("scheme", ["wfbp", "priority", "nonsequential"])
 @pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("placement", ["end", "start", "bucket"])
 def test_loopback_synchronous_baselines(scheme, world, placement):
     """Updates of iteration t visible from t+1 (oracle lag 1); priority uses
-    partition_by_size blocks (1000-element buckets cut into 334/333/333)."""
+    partition_by_size blocks (1000-element buckets cut into 334/333/333);
+    nonsequential picks among those and fused blocks (startup cost 500 us)."""
     iters = 10
     masters, params, theta0, decisions, buckets, _ = S.run_loopback(
         world, iters, placement=placement, scheme=scheme,
-        cuda_graphs=placement != "bucket",
-        partition_size=400 if scheme == "priority" else 10**9)
+        cuda_graphs=placement != "bucket", startup_us=500,
+        partition_size=10**9 if scheme == "wfbp" else 400)
     d0 = decisions[0]
     assert all(u["merge_count"] == 1 for d in d0 for u in d["update_events"])
     want_m, want_p = S.oracle_theta(theta0, d0, world, iters, lag=1)

@@ -164,3 +164,25 @@ def test_preserver_golden(golden_inputs):
             seq = D.BatchSequence(tuple(row["k_values"]), row["batch"])
             assert D.check_sequence(seq, walk) == (row["preserved"], row["ratio"],
                                                    row["merged"], row["base"])
+
+
+def test_nonsequential_matches_reference_goldens():
+    """baseline_nonsequential (scheduler.py:421-472): byte-identical decision
+    streams and block structures vs the reference run (tests/golden/
+    make_nonseq_golden.py); its scoring rule equals the reference simulator's
+    total time (sync_schedule_time_us vs simulate(), WFBP order)."""
+    import hashlib
+    import json as _json
+    from pathlib import Path as _P
+    import paper_2503_16815_b200 as D
+    cases = _json.loads((_P(__file__).parent / "golden" / "nonsequential.json").read_text())
+    for c in cases:
+        prof, cl = D.profile_from_dict(c["profile"]), D.cluster_from_dict(c["cluster"])
+        cfg = D.PartitionConfig(partition_size=c["partition_size"],
+                                comm_startup_us=c["comm_startup_us"])
+        s = D.build_schedule("nonsequential", prof, cl, cfg, c["iterations"])
+        text = "".join(_json.dumps(d.to_dict(), sort_keys=True) + "\n" for d in s.decisions)
+        assert hashlib.sha256(text.encode()).hexdigest() == c["want"]["sha256"], c["profile"]["name"]
+        assert [b.param_count for b in s.profile.buckets] == c["want"]["blocks"]
+        assert D.sync_schedule_time_us(prof, cl.fast_link, [b.id for b in prof.buckets],
+                                       c["iterations"]) == c["want"]["wfbp_total_us"]
