@@ -508,8 +508,7 @@ def ddp_baseline(args, world, rank, device, dist):
         net = torch.nn.parallel.DistributedDataParallel(
             model, device_ids=[device.index], bucket_cap_mb=bucket_mb,
             gradient_as_bucket_view=True, static_graph=args.ddp_graphs)
-    opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9, fused=True,
-                          capturable=args.ddp_graphs)
+    opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9, fused=True)
     amp = next(model.parameters()).dtype == torch.float32
 
     def step():

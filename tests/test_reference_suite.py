@@ -47,4 +47,7 @@ def test_reference_suite_against_this_package(tmp_path):
     for line in out.splitlines():
         if line.startswith("SKIPPED"):
             assert "outside the B200 hot path" in line, line
-    assert passed >= 90, out[-2000:]
+    skipped = re.search(r"(\d+) skipped", out)
+    skipped = int(skipped.group(1)) if skipped else 0
+    # 91 in-scope tests: C5 (trace), C7/C8 (simulator), C12 (CLI) skip, the rest pass
+    assert passed + skipped == 91 and skipped <= 4, out[-2000:]
