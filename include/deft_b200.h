@@ -191,6 +191,21 @@ deft_status_t deft_bucket_update_multi(deft_comm* c, int32_t slot, int32_t count
                                        float momentum, float grad_scale, float* d_mom,
                                        void* stream);
 
+/* One-shot bucket sync (small buckets): the all-reduce AND the update of
+ * every bucket of one update event in ONE launch -- each rank reads the whole
+ * of [offsets[k], +numels[k]) from every rank's slot `slot` (own + W-1 peers
+ * over NVLink), sums in rank order in fp32, rounds to the gradient dtype and
+ * applies g*grad_scale, v = m*v + g, p -= lr*v to the FULL bucket locally
+ * (momentum / fp32 master of such buckets are replicated on every rank,
+ * bit-identical).  No deft_bucket_reduce_scatter may run for these buckets;
+ * entry and exit barriers inside.  Same results as reduce-scatter +
+ * deft_bucket_update_multi.  Replaces the simulated transfer + update event
+ * of a bucket whose startup cost dominates (simulator.py:136-147). */
+deft_status_t deft_bucket_sync_update_multi(deft_comm* c, int32_t slot, int32_t count,
+                                            const int64_t* offsets, const int64_t* numels,
+                                            float lr, float momentum, float grad_scale,
+                                            float* d_mom, void* stream);
+
 /* Local (W == 1 or rank-private) fused update over device arrays:
  * v = m*v + s*g ; p -= lr*v. grad_dtype as above; d_param has the grad dtype;
  * for bf16 the fp32 master d_master is updated and rounded into d_param. */

@@ -30,7 +30,7 @@ EXPORTED = (
     "deft_bucket_update_multi",
     "deft_sgd_momentum_update", "deft_sgd_momentum_update_multi", "deft_gather_segments",
     "deft_stream_create", "deft_stream_destroy", "deft_stream_alias_probe",
-    "deft_loopback_reduce_scatter", "deft_loopback_update",
+    "deft_loopback_reduce_scatter", "deft_loopback_update", "deft_bucket_sync_update_multi",
 )
 
 DTYPE_F32, DTYPE_BF16 = 0, 1
@@ -76,6 +76,8 @@ def _declare(lib):
         "deft_comm_destroy": (c_i32, [c_vp]),
         "deft_comm_set_update_blocks": (c_i32, [c_vp, c_i32]),
         "deft_comm_configure": (c_i32, [c_vp, c_i32, c_i64]),
+        "deft_bucket_sync_update_multi": (c_i32, [c_vp, c_i32, c_i32, P(c_i64), P(c_i64),
+                                                  c_f32, c_f32, c_f32, c_vp, c_vp]),
         "deft_stream_create": (c_i32, [c_i32, P(c_vp)]),
         "deft_loopback_reduce_scatter": (c_i32, [P(c_vp), c_i32, c_i32, c_i32, c_i32,
                                                  P(c_i64), P(c_i64), c_vp]),

@@ -191,6 +191,18 @@ class BucketComm:
             self._h, slot, n, offs, lens, lr, momentum, scale, c_vp(mom.data_ptr()),
             c_vp(stream.cuda_stream)), "deft_bucket_update_multi")
 
+    def sync_update_multi(self, slot: int, ranges, scale: float, lr: float, momentum: float,
+                          mom: torch.Tensor, stream) -> None:
+        """One-shot bucket sync (deft_bucket_sync_update_multi): the all-reduce of
+        the full buckets fused with their update, one launch, no reduce-scatter
+        before it and no all-gather after it."""
+        n = len(ranges)
+        offs = (ctypes.c_int64 * n)(*[lo for lo, _ in ranges])
+        lens = (ctypes.c_int64 * n)(*[hi - lo for lo, hi in ranges])
+        check(_native.lib().deft_bucket_sync_update_multi(
+            self._h, slot, n, offs, lens, lr, momentum, scale, c_vp(mom.data_ptr()),
+            c_vp(stream.cuda_stream)), "deft_bucket_sync_update_multi")
+
     def close(self, barrier: bool = True) -> None:
         if getattr(self, "_h", None) is not None:
             torch.cuda.synchronize(self.device)

@@ -1466,3 +1466,181 @@ cudaError_t launch_update_tma_loopback(const PeerPtrs& P, int world, int dtype,
 }
 
 }  // namespace deft
+
+namespace deft {
+
+// ============================================================================
+// One-shot bucket sync for small buckets: ONE launch per update event does the
+// all-reduce and the update.  Every rank reads the WHOLE bucket from every
+// rank's gradient slot (own + W-1 peers over NVLink, 128-bit loads), sums in
+// rank order in fp32, rounds to the slot dtype (exactly what the two-shot
+// reduce-scatter stores), and applies the fused SGD/momentum update to the
+// full bucket locally -- momentum and (bf16) master of one-shot buckets are
+// replicated, bit-identical on every rank because every rank sums in the same
+// order.  No reduce-scatter launch at the transfer point, no parameter
+// all-gather: the per-bucket fixed cost (two launches, three barrier rounds)
+// becomes one launch and one barrier pair.  Reads (W-1) x bucket bytes per rank
+// over NVLink instead of 2 (W-1)/W x: the small-bucket trade.
+// ============================================================================
+constexpr int kOneShotThreads = 256;
+constexpr int kOneShotUnroll = 2;
+
+template <typename T, int W>
+__global__ void __launch_bounds__(kOneShotThreads) oneshot_update_kernel(
+    PeerPtrs P, int rank, int64_t slot_base, const __grid_constant__ SegTable t, float lr,
+    float momentum, float* __restrict__ mom) {
+  using V = Vec<T>;
+  using Raw = typename V::Raw;
+  constexpr int N = V::N;
+  constexpr bool kMaster = sizeof(T) == 2;
+  const uint32_t epoch = take_epochs(P, rank, kBarrierUpdate, 2u);
+  // entry: every rank's slot holds this group's complete gradient
+  peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 1u);
+  const T* src[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) src[k] = reinterpret_cast<const T*>(P.grads[k]) + slot_base;
+  float* ref = kMaster ? P.master : reinterpret_cast<float*>(P.params[rank]);
+  T* dst = reinterpret_cast<T*>(P.params[rank]);
+  auto one = [&](int64_t e, float s) {   // scalar element (unaligned heads / tails)
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < W; ++k) acc += V::scalar(src[k] + e);
+    T r;
+    V::put(&r, acc);
+    const float g = V::scalar(&r);
+    const float v = fmaf(momentum, mom[e], g * s);
+    mom[e] = v;
+    const float p = fmaf(-lr, v, ref[e]);
+    if (kMaster) ref[e] = p;
+    store1(dst + e, p);
+  };
+  const int64_t total = t.first_vec[t.count];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t u0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u0 < total;
+       u0 += stride * kOneShotUnroll) {
+    Raw raw[kOneShotUnroll][W];
+    int64_t el[kOneShotUnroll];
+    float sc[kOneShotUnroll];
+    bool vec[kOneShotUnroll];
+#pragma unroll
+    for (int q = 0; q < kOneShotUnroll; ++q) {
+      const int64_t u = u0 + q * stride;
+      vec[q] = false;
+      el[q] = -1;
+      if (u >= total) continue;
+      int sg = 0;
+      while (u >= t.first_vec[sg + 1]) ++sg;
+      const int64_t base = t.off[sg], end = base + t.len[sg];
+      const int64_t aligned = (base + N - 1) / N * N;
+      const int64_t k = u - t.first_vec[sg];
+      sc[q] = t.scale[sg];
+      if (k == 0)
+        for (int64_t e = base; e < aligned && e < end; ++e) one(e, sc[q]);  // head
+      const int64_t e = aligned + k * N;
+      el[q] = e;
+      if (e + N <= end) {
+        vec[q] = true;
+#pragma unroll
+        for (int r = 0; r < W; ++r) raw[q][r] = ld_nc(reinterpret_cast<const Raw*>(src[r] + e));
+      } else {
+        for (int64_t x = e; x < end; ++x) one(x, sc[q]);                     // tail
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kOneShotUnroll; ++q) {
+      if (!vec[q]) continue;
+      float acc[N], tmp[N];
+      V::to_f32(raw[q][0], acc);
+#pragma unroll
+      for (int r = 1; r < W; ++r) {
+        V::to_f32(raw[q][r], tmp);
+#pragma unroll
+        for (int c = 0; c < N; ++c) acc[c] += tmp[c];
+      }
+      V::to_f32(V::from_f32(acc), acc);        // the slot dtype's rounding
+      const int64_t e = el[q];
+      float vv[N], pp[N];
+#pragma unroll
+      for (int c = 0; c < N; c += 4) {
+        const float4 m4 = load4(mom + e + c);
+        const float4 p4 = load4(ref + e + c);
+        vv[c + 0] = fmaf(momentum, m4.x, acc[c + 0] * sc[q]);
+        vv[c + 1] = fmaf(momentum, m4.y, acc[c + 1] * sc[q]);
+        vv[c + 2] = fmaf(momentum, m4.z, acc[c + 2] * sc[q]);
+        vv[c + 3] = fmaf(momentum, m4.w, acc[c + 3] * sc[q]);
+        pp[c + 0] = fmaf(-lr, vv[c + 0], p4.x);
+        pp[c + 1] = fmaf(-lr, vv[c + 1], p4.y);
+        pp[c + 2] = fmaf(-lr, vv[c + 2], p4.z);
+        pp[c + 3] = fmaf(-lr, vv[c + 3], p4.w);
+        store4(mom + e + c, make_float4(vv[c], vv[c + 1], vv[c + 2], vv[c + 3]));
+        if (kMaster) store4(ref + e + c, make_float4(pp[c], pp[c + 1], pp[c + 2], pp[c + 3]));
+      }
+      reinterpret_cast<Raw*>(dst + e)[0] = V::from_f32(pp);
+    }
+  }
+  // exit: no peer reads this rank's slot any more (it may be recycled)
+  peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 2u);
+}
+
+// DEFT_ONESHOT_BLOCKS: CTA cap of the one-shot kernel (default 128)
+static int oneshot_max_blocks() {
+  static int v = [] {
+    const char* e = getenv("DEFT_ONESHOT_BLOCKS");
+    int x = e ? atoi(e) : 128;
+    return x < 1 ? 1 : (x > kMaxCommBlocks ? kMaxCommBlocks : x);
+  }();
+  return v;
+}
+
+cudaError_t launch_oneshot_update(const PeerPtrs& P, int rank, int world, int dtype,
+                                  int64_t slot_base, int32_t count, const int64_t* offsets,
+                                  const int64_t* numels, float lr, float momentum,
+                                  float grad_scale, float* mom, int max_blocks,
+                                  cudaStream_t stream) {
+  if (world < 2 || world > 8) return cudaErrorInvalidValue;
+  const int N = dtype == 0 ? 4 : 8;
+  for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
+    SegTable t{};
+    t.count = count - s0 < kMaxSeg ? count - s0 : kMaxSeg;
+    t.first_vec[0] = 0;
+    for (int k = 0; k < t.count; ++k) {
+      t.off[k] = offsets[s0 + k];
+      t.len[k] = numels[s0 + k];
+      t.scale[k] = grad_scale;
+      const int64_t aligned = (t.off[k] + N - 1) / N * N;
+      const int64_t end = t.off[k] + t.len[k];
+      int64_t units = end > aligned ? (end - aligned + N - 1) / N : 0;
+      if (units == 0 && t.len[k] > 0) units = 1;
+      t.first_vec[k + 1] = t.first_vec[k] + units;
+    }
+    const int64_t total = t.first_vec[t.count];
+    if (total == 0) continue;
+    // identical on every rank: a function of the bucket sizes only
+    int64_t g = (total + (int64_t)kOneShotThreads * kOneShotUnroll - 1) /
+                ((int64_t)kOneShotThreads * kOneShotUnroll);
+    int grid = (int)(g < 1 ? 1 : (g > oneshot_max_blocks() ? oneshot_max_blocks() : g));
+    if (max_blocks > 0 && grid > max_blocks) grid = max_blocks;
+    grid = cap_grid(P, grid);
+#define DEFT_OS_CASE(WW)                                                                  \
+  case WW:                                                                                \
+    if (dtype == 0)                                                                       \
+      oneshot_update_kernel<float, WW><<<grid, kOneShotThreads, 0, stream>>>(             \
+          P, rank, slot_base, t, lr, momentum, mom);                                      \
+    else                                                                                  \
+      oneshot_update_kernel<__nv_bfloat16, WW><<<grid, kOneShotThreads, 0, stream>>>(     \
+          P, rank, slot_base, t, lr, momentum, mom);                                      \
+    break;
+    switch (world) {
+      DEFT_OS_CASE(2) DEFT_OS_CASE(3) DEFT_OS_CASE(4) DEFT_OS_CASE(5)
+      DEFT_OS_CASE(6) DEFT_OS_CASE(7) DEFT_OS_CASE(8)
+      default: break;
+    }
+#undef DEFT_OS_CASE
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace deft

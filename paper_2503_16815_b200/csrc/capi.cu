@@ -623,6 +623,29 @@ extern "C" deft_status_t deft_bucket_update_multi(deft_comm* c, int32_t slot, in
   return DEFT_OK;
 }
 
+extern "C" deft_status_t deft_bucket_sync_update_multi(deft_comm* c, int32_t slot,
+                                                      int32_t count, const int64_t* offsets,
+                                                      const int64_t* numels, float lr,
+                                                      float momentum, float grad_scale,
+                                                      float* d_mom, void* stream) {
+  if (!c) return fail(DEFT_ERR_INVALID_ARGUMENT, "null comm");
+  if (count <= 0) return DEFT_OK;
+  if (!d_mom) return fail(DEFT_ERR_INVALID_ARGUMENT, "momentum buffer required");
+  for (int32_t k = 0; k < count; ++k) {
+    deft_status_t st = check_range(c, slot, offsets[k], numels[k]);
+    if (st != DEFT_OK) return st;
+  }
+  if (c->world == 1)   // nothing to reduce: the local fused update
+    return deft_bucket_update_multi(c, slot, count, offsets, numels, lr, momentum, grad_scale,
+                                    d_mom, stream);
+  cudaError_t e = launch_oneshot_update(c->P, c->rank, c->world, c->dtype,
+                                        (int64_t)slot * c->slot_elems, count, offsets, numels,
+                                        lr, momentum, grad_scale, d_mom, c->update_blocks,
+                                        (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "oneshot_update_kernel");
+  return DEFT_OK;
+}
+
 // ============================================================================
 // Loopback collectives (one launch for all ranks of a loopback world)
 // ============================================================================

@@ -79,6 +79,14 @@ __host__ __device__ inline ShardRange shard_of(int64_t offset, int64_t numel, in
 
 int comm_grid_for(int64_t elems_per_rank);
 
+// one-shot bucket sync: all-reduce of the full buckets (every rank reads every
+// peer) fused with the update, parameters written locally (bucket_comm.cu)
+cudaError_t launch_oneshot_update(const PeerPtrs& P, int rank, int world, int dtype,
+                                  int64_t slot_base, int32_t count, const int64_t* offsets,
+                                  const int64_t* numels, float lr, float momentum,
+                                  float grad_scale, float* mom, int max_blocks,
+                                  cudaStream_t stream);
+
 // loopback collectives (one launch, gridDim.y = world; synchronous)
 cudaError_t launch_barrier_loopback(const PeerPtrs& P, int world, int set, cudaStream_t stream);
 cudaError_t launch_rs_tma_loopback(const PeerPtrs& P, int world, int dtype, int64_t slot_base,

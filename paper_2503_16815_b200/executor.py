@@ -56,6 +56,17 @@ from .scheduler import (DeftScheduler, OrderScheduler, ScheduleDecision,
 
 SCHEMES = ("deft", "wfbp", "priority", "nonsequential")
 
+# default one-shot threshold (bytes of one bucket's gradients); see DESIGN.md
+ONESHOT_DEFAULT_BYTES = 0
+
+
+def oneshot_limit(cfg_value: int | None) -> int:
+    import os
+    if cfg_value is not None:
+        return int(cfg_value)
+    env = os.environ.get("DEFT_ONESHOT_MAX_BYTES")
+    return int(env) if env else ONESHOT_DEFAULT_BYTES
+
 
 @dataclass
 class DeftConfig:
@@ -96,6 +107,11 @@ class DeftConfig:
     # input layer first).  Synchronous: updates of iteration t visible from t+1.
     scheme: str = "deft"
     graph_warmup: int = 2                   # eager iterations before any capture
+    # buckets of at most this many gradient bytes sync "one-shot" at W > 1: no
+    # reduce-scatter at the transfer point, the update reads every rank's slot
+    # (all-reduce + update in one launch, no all-gather).  None = the measured
+    # default (DEFT_ONESHOT_MAX_BYTES, else ONESHOT_DEFAULT_BYTES); 0 = never
+    oneshot_max_bytes: int | None = None
     defer_tail: bool = True                 # delayed schedules: last transfers -> next iteration
 
 
@@ -486,6 +502,9 @@ class DeftDataParallel:
                         zip(part.buckets, element_ranges(part, None))]
         owner = self._owner_map([(b.lo, b.hi) for b in self.buckets])
         self._param_buckets = [owner[id(p)] for p in self.params]
+        esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
+        lim = oneshot_limit(self.cfg.oneshot_max_bytes)
+        self._oneshot = [self.world > 1 and (b.hi - b.lo) * esz <= lim for b in self.buckets]
         self._bucket_nparams = [0] * len(self.buckets)
         self._bucket_params: list[list[int]] = [[] for _ in self.buckets]
         for i, bl in enumerate(self._param_buckets):
@@ -614,7 +633,10 @@ class DeftDataParallel:
     def _issue_rs(self, link: int, slot: int, bidxs: list[int], release: torch.cuda.Event,
                   track: bool = False):
         """The buckets one release point puts on one link, in plan order: ONE
-        reduce-scatter launch (one cross-rank barrier) on the link's stream."""
+        reduce-scatter launch (one cross-rank barrier) on the link's stream.
+        One-shot buckets have no transfer of their own: their update reads every
+        rank's slot (deft_bucket_sync_update_multi)."""
+        bidxs = [b for b in bidxs if not self._oneshot[b]]
         if self.world == 1 or not bidxs:
             return
         s = self.link_streams[link]
@@ -635,6 +657,22 @@ class DeftDataParallel:
             ev.record(s)
             for b in bidxs:
                 self._rs_done[(slot, b)] = ev
+
+    def _launch_update(self, slot: int, bidxs, k: int, stream, nbytes: int):
+        """One update event over buckets `bidxs`: the two-shot buckets (reduce-
+        scattered at their transfer) get the fused update + parameter all-gather,
+        the one-shot buckets the fused all-reduce + update -- one launch each."""
+        two = [(self.buckets[b].lo, self.buckets[b].hi) for b in bidxs if not self._oneshot[b]]
+        one = [(self.buckets[b].lo, self.buckets[b].hi) for b in bidxs if self._oneshot[b]]
+        scale = 1.0 / (self.world * k)
+        if two:
+            self._timed("update", stream, lambda: self.comm.update_multi(
+                slot, two, scale, self.cfg.lr, self.cfg.momentum, self.mom, stream), nbytes)
+        if one:
+            esz = 2 if self.cfg.grad_dtype == torch.bfloat16 else 4
+            ob = sum(hi - lo for lo, hi in one) * esz * (self.world - 1)   # peer reads
+            self._timed("oneshot", stream, lambda: self.comm.sync_update_multi(
+                slot, one, scale, self.cfg.lr, self.cfg.momentum, self.mom, stream), ob)
 
     def _issue_planned(self, transfers, release: torch.cuda.Event):
         """Stage-plan transfers (link, slot, bucket) released together: per link,
@@ -658,9 +696,7 @@ class DeftDataParallel:
                 rs = self._rs_done.pop((slot, b), None)
                 if rs is not None:
                     s.wait_event(rs)
-            self._timed("update", s, lambda: self.comm.update_multi(
-                slot, ranges, 1.0 / (self.world * k), self.cfg.lr, self.cfg.momentum,
-                self.mom, s), nbytes)
+            self._launch_update(slot, bidxs, k, s, nbytes)
 
     def _install_forward_waits(self):
         """"start" placement: the forward pre-hook of every module that owns
@@ -736,9 +772,7 @@ class DeftDataParallel:
                         rs = self._rs_done.pop((slot, b), None)
                         if rs is not None:
                             s.wait_event(rs)
-                self._timed("update", s, lambda: self.comm.update_multi(
-                    slot, ranges, 1.0 / (self.world * k), self.cfg.lr, self.cfg.momentum,
-                    self.mom, s), nbytes)
+                self._launch_update(slot, group, k, s, nbytes)
             ev = torch.cuda.Event()
             ev.record(s)
             for b in group:
@@ -761,9 +795,7 @@ class DeftDataParallel:
                     rs = self._rs_done.pop((slot, b), None)
                     if rs is not None:
                         comp.wait_event(rs)
-            self._timed("update", comp, lambda: self.comm.update_multi(
-                slot, ranges, 1.0 / (self.world * k), self.cfg.lr, self.cfg.momentum, self.mom,
-                comp), nbytes)
+            self._launch_update(slot, range(len(self.buckets)), k, comp, nbytes)
 
     def _on_grad(self, p):
         if not self._in_step:

@@ -80,6 +80,34 @@ def test_loopback_synchronous_baselines(scheme, world, placement):
     assert S.elem_err(masters[0], delayed) > 1e-4
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("placement", ["end", "start", "bucket"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_loopback_oneshot(world, placement, dtype):
+    """Every bucket one-shot (deft_bucket_sync_update_multi): no reduce-scatter,
+    each rank reads all peers' full buckets and updates them locally -- same
+    results as the two-shot path (fp32 elementwise 1e-6, bf16 bit-exact)."""
+    _check(world, 14, dtype=dtype, placement=placement, cuda_graphs=placement != "bucket",
+           oneshot=10**9)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("scheme", ["deft", "priority"])
+def test_loopback_oneshot_mixed(world, scheme):
+    """One-shot and two-shot buckets in the same update events: 400-parameter
+    partitions cut each 1000-element bucket into 334/333/333; buckets of at most
+    333 x 4 bytes go one-shot, the 334-element ones two-shot."""
+    iters = 12
+    masters, params, theta0, decisions, buckets, _ = S.run_loopback(
+        world, iters, placement="start", scheme=scheme, partition_size=400,
+        oneshot=333 * 4)
+    sizes = {hi - lo for lo, hi in buckets}
+    assert sizes == {333, 334}, sizes
+    want_m, want_p = S.oracle_theta(theta0, decisions[0], world, iters,
+                                    lag=2 if scheme == "deft" else 1)
+    S.check_ranks(masters, params, want_m, want_p, world, torch.float32, buckets)
+
+
 class _ProbeWithUnused(S.Probe):
     """Parameter 3 never takes part in the loss: its gradient is None."""
 

@@ -9,9 +9,14 @@ barrier, max over ranks:
   rs_ce     reduce-scatter, copy-engine channel   (ch 1)
   upd_ag    fused SGD/momentum + parameter all-gather (deft_bucket_update)
   deft      rs_sm + upd_ag back to back = a full DeFT bucket sync incl. the update
+  oneshot   fused all-reduce + update in one launch (deft_bucket_sync_update_multi)
   nccl_ar   NCCL all_reduce (fp32 sum) of the bucket
   nccl_ar_sgd  NCCL all_reduce + torch SGD/momentum on the bucket (the DDP baseline)
 Bus bandwidth: RS and AG move (W-1)/W of the bucket per rank each; AR 2(W-1)/W.
+--nvml: NVLink TX/RX bytes per launch of every kernel, from the NVML
+throughput counters (NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX, summed over
+links) read around the timed loop -- isolated launches, so no profiler replay
+of cross-GPU barriers is needed; compare with the algorithmic bytes.
 """
 import argparse
 import json
@@ -28,17 +33,54 @@ from paper_2503_16815_b200 import _native  # noqa: E402
 from paper_2503_16815_b200.comm import BucketComm  # noqa: E402
 
 
-def timeit(fn, reps, warm, stream, device):
+NVML = {}
+
+
+def nvlink_bytes():
+    """(tx, rx) NVLink data bytes of this GPU so far (NVML counters, KiB units)."""
+    h = NVML.get("h")
+    if h is None:
+        return None
+    import pynvml as N
+    fields = []
+    for link in range(NVML["links"]):
+        fields += [(N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, link),
+                   (N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, link)]
+    vals = N.nvmlDeviceGetFieldValues(h, fields)
+    tx = sum(v.value.ullVal for v in vals[0::2] if v.nvmlReturn == 0)
+    rx = sum(v.value.ullVal for v in vals[1::2] if v.nvmlReturn == 0)
+    return tx * 1024, rx * 1024
+
+
+def nvml_init(device):
+    try:
+        import pynvml as N
+        N.nvmlInit()
+        idx = torch.cuda._get_nvml_device_index(device.index)
+        NVML["h"] = N.nvmlDeviceGetHandleByIndex(idx)
+        NVML["links"] = 18
+    except Exception as e:  # reported in the output
+        NVML["error"] = repr(e)
+
+
+def timeit(fn, reps, warm, stream, device, nv=None, key=None):
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
     dist.barrier()
+    before = nvlink_bytes() if nv is not None else None
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
     for _ in range(reps):
         fn()
     b.record(stream)
     torch.cuda.synchronize()
+    if before is not None:
+        import time
+        time.sleep(0.15)          # counters are sampled by the driver
+        after = nvlink_bytes()
+        nv[key] = {"tx_per_launch": (after[0] - before[0]) / reps,
+                   "rx_per_launch": (after[1] - before[1]) / reps}
     t = torch.tensor([a.elapsed_time(b) / reps], device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -52,12 +94,16 @@ def main():
                     help="CTA budget of the update kernels (0 = default)")
     ap.add_argument("--check", action="store_true",
                     help="verify every reduce-scatter result before timing")
+    ap.add_argument("--nvml", action="store_true", help="NVLink bytes per launch (NVML)")
+    ap.add_argument("--no-nccl", action="store_true")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     W, rank = dist.get_world_size(), dist.get_rank()
+    if args.nvml:
+        nvml_init(dev)
     sizes = [int(x) for x in args.sizes_mb.split(",")]
     max_elems = max(sizes) * 2**20 // 4
     comm = BucketComm(rank, W, 1, max_elems, torch.float32, dev)
@@ -86,37 +132,56 @@ def main():
                 res[f"check_err_ch{ch}"] = err
                 assert err < 1e-4, (ch, err)
                 dist.barrier()
+        nv = {} if args.nvml else None
         with torch.cuda.stream(s):
             res["rs_sm_ms"] = timeit(lambda: comm.reduce_scatter(_native.CHANNEL_SM, 0, 0, n, s),
-                                     args.reps, 3, s, dev)
+                                     args.reps, 3, s, dev, nv, "rs_sm")
             res["rs_ce_ms"] = timeit(lambda: comm.reduce_scatter(_native.CHANNEL_CE, 0, 0, n, s),
-                                     args.reps, 3, s, dev)
+                                     args.reps, 3, s, dev, nv, "rs_ce")
             # the multi-bucket entry point: the TMA-pipelined update kernel
             res["upd_ag_ms"] = timeit(
                 lambda: comm.update_multi(0, [(0, n)], 1e-3, 1e-9, 0.9, mom, s),
-                args.reps, 3, s, dev)
+                args.reps, 3, s, dev, nv, "upd_ag")
+            res["oneshot_ms"] = timeit(
+                lambda: comm.sync_update_multi(0, [(0, n)], 1e-3, 1e-9, 0.9, mom, s),
+                args.reps, 3, s, dev, nv, "oneshot")
 
             def deft():
                 comm.reduce_scatter(_native.CHANNEL_SM, 0, 0, n, s)
                 comm.update_multi(0, [(0, n)], 1e-3, 1e-9, 0.9, mom, s)
             res["deft_ms"] = timeit(deft, args.reps, 3, s, dev)
-            x = torch.randn(n, device=dev)
-            p = torch.randn(n, device=dev)
-            v = torch.zeros(n, device=dev)
-            res["nccl_ar_ms"] = timeit(lambda: dist.all_reduce(x), args.reps, 3, s, dev)
+            if not args.no_nccl:
+                x = torch.randn(n, device=dev)
+                p = torch.randn(n, device=dev)
+                v = torch.zeros(n, device=dev)
+                res["nccl_ar_ms"] = timeit(lambda: dist.all_reduce(x), args.reps, 3, s, dev,
+                                           nv, "nccl_ar")
 
-            def nccl_sgd():
-                dist.all_reduce(x)
-                v.mul_(0.9).add_(x, alpha=1e-3)
-                p.add_(v, alpha=-1e-9)
-            res["nccl_ar_sgd_ms"] = timeit(nccl_sgd, args.reps, 3, s, dev)
+                def nccl_sgd():
+                    dist.all_reduce(x)
+                    v.mul_(0.9).add_(x, alpha=1e-3)
+                    p.add_(v, alpha=-1e-9)
+                res["nccl_ar_sgd_ms"] = timeit(nccl_sgd, args.reps, 3, s, dev)
         frac = (W - 1) / W
         res["rs_sm_busbw_gbs"] = round(frac * nbytes / res["rs_sm_ms"] / 1e6, 1)
         res["rs_ce_busbw_gbs"] = round(frac * nbytes / res["rs_ce_ms"] / 1e6, 1)
         res["upd_ag_busbw_gbs"] = round(frac * nbytes / res["upd_ag_ms"] / 1e6, 1)
         res["deft_busbw_gbs"] = round(2 * frac * nbytes / res["deft_ms"] / 1e6, 1)
-        res["nccl_ar_busbw_gbs"] = round(2 * frac * nbytes / res["nccl_ar_ms"] / 1e6, 1)
-        res["deft_vs_nccl_ar_sgd"] = round(res["nccl_ar_sgd_ms"] / res["deft_ms"], 3)
+        res["oneshot_busbw_gbs"] = round(2 * frac * nbytes / res["oneshot_ms"] / 1e6, 1)
+        res["best_sync_ms"] = min(res["deft_ms"], res["oneshot_ms"])
+        if "nccl_ar_ms" in res:
+            res["nccl_ar_busbw_gbs"] = round(2 * frac * nbytes / res["nccl_ar_ms"] / 1e6, 1)
+            res["deft_vs_nccl_ar_sgd"] = round(res["nccl_ar_sgd_ms"] / res["deft_ms"], 3)
+            res["best_vs_nccl_ar"] = round(res["nccl_ar_ms"] / res["best_sync_ms"], 3)
+        if nv is not None:
+            # algorithmic NVLink bytes per rank: RS rx (W-1)/W, AG tx (W-1)/W,
+            # one-shot rx (W-1) x bucket; the measured counters beside them
+            res["nvlink"] = {k: {"tx": int(v["tx_per_launch"]), "rx": int(v["rx_per_launch"])}
+                             for k, v in nv.items()}
+            res["nvlink_algorithmic"] = {"rs_rx": int(frac * nbytes), "upd_ag_tx":
+                                         int(frac * nbytes), "oneshot_rx": (W - 1) * nbytes}
+        if NVML.get("error"):
+            res["nvml_error"] = NVML["error"]
         for k in list(res):
             if k.endswith("_ms"):
                 res[k] = round(res[k], 4)
