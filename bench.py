@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--start-grouping", default="auto", choices=["auto", "size", "timed"],
                     help="how start-placement updates are grouped into launches")
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs")
+    ap.add_argument("--defer", default="last", choices=["last", "predicted", "none"],
+                    help="graph mode: which fresh transfers start with the next iteration "
+                         "(DeftConfig.defer_tail)")
     ap.add_argument("--bucket-mb", type=float, default=None,
                     help="partition size in MB of fp32 (default: the reference's 6.5M params)")
     ap.add_argument("--links", default="both", choices=["both", "sm", "ce"],
@@ -625,6 +628,7 @@ def main():
                        update_placement=args.update_placement,
                        update_blocks=args.update_blocks, scheme=args.scheme,
                        start_grouping=args.start_grouping,
+                       defer_tail=False if args.defer == "none" else args.defer,
                        autocast_dtype=None if args.model == "gpt2" else torch.bfloat16,
                        partition=D.PartitionConfig(partition_size=psize, mu=1.0))
     ddp = D.DeftDataParallel(model, cfg)

@@ -526,10 +526,10 @@ struct SegTable {
   int32_t count;
 };
 
-template <typename T>
+template <typename T, int U>
 __global__ void __launch_bounds__(kLocalThreads) sgd_local_kernel(
     const T* __restrict__ grad, T* __restrict__ param, float* __restrict__ master,
-    float* __restrict__ mom, SegTable t, float lr, float momentum) {
+    float* __restrict__ mom, const __grid_constant__ SegTable t, float lr, float momentum) {
   using V = Vec<T>;
   constexpr bool kMaster = sizeof(T) == 2;  // bf16 params: fp32 master is authoritative
   float* ref = kMaster ? master : reinterpret_cast<float*>(param);
@@ -543,37 +543,75 @@ __global__ void __launch_bounds__(kLocalThreads) sgd_local_kernel(
     if (kMaster) ref[e] = p;
     store1(param + e, p);
   };
-  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < total; u += stride) {
-    while (u >= t.first_vec[seg + 1]) ++seg;
-    // unit u covers 4 consecutive elements of segment `seg`, from its aligned start
-    const int64_t base = t.off[seg];
-    const int64_t end = base + t.len[seg];
-    const int64_t aligned = (base + 3) / 4 * 4;
-    const int64_t k = u - t.first_vec[seg];
-    const float s = t.scale[seg];
-    if (k == 0 && aligned > base) {  // unit 0 also owns the unaligned head
-      for (int64_t e = base; e < aligned && e < end; ++e) one(e, s);
+  // U units per thread per pass (unit u covers 4 consecutive elements of its
+  // segment from the segment's aligned start): all 3U 16-byte loads are issued
+  // before the first use, so each thread keeps U x 48 B of HBM reads in flight
+  for (int64_t u0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u0 < total;
+       u0 += stride * U) {
+    float4 g4[U], m4[U], p4[U];
+    int64_t el[U];
+    float sc[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int64_t u = u0 + q * stride;
+      el[q] = -1;
+      if (u >= total) continue;
+      while (u >= t.first_vec[seg + 1]) ++seg;   // u grows: seg only moves forward
+      const int64_t base = t.off[seg];
+      const int64_t end = base + t.len[seg];
+      const int64_t aligned = (base + 3) / 4 * 4;
+      const int64_t k = u - t.first_vec[seg];
+      sc[q] = t.scale[seg];
+      if (k == 0 && aligned > base) {  // unit 0 also owns the unaligned head
+        for (int64_t e = base; e < aligned && e < end; ++e) one(e, sc[q]);
+      }
+      const int64_t e = aligned + k * 4;
+      if (e + 4 <= end) {
+        el[q] = e;
+        g4[q] = load4(grad + e);
+        m4[q] = load4(mom + e);
+        p4[q] = load4(ref + e);
+      } else {
+        for (int64_t x = e; x < end; ++x) one(x, sc[q]);  // tail
+      }
     }
-    const int64_t e = aligned + k * 4;
-    if (e + 4 <= end) {
-      const float4 g4 = load4(grad + e);
-      float4 m4 = load4(mom + e);
-      float4 p4 = load4(ref + e);
-      m4.x = fmaf(momentum, m4.x, g4.x * s);
-      m4.y = fmaf(momentum, m4.y, g4.y * s);
-      m4.z = fmaf(momentum, m4.z, g4.z * s);
-      m4.w = fmaf(momentum, m4.w, g4.w * s);
-      p4.x = fmaf(-lr, m4.x, p4.x);
-      p4.y = fmaf(-lr, m4.y, p4.y);
-      p4.z = fmaf(-lr, m4.z, p4.z);
-      p4.w = fmaf(-lr, m4.w, p4.w);
-      store4(mom + e, m4);
-      if (kMaster) store4(ref + e, p4);
-      store4(param + e, p4);
-    } else {
-      for (int64_t x = e; x < end; ++x) one(x, s);  // tail
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      if (el[q] < 0) continue;
+      const float s = sc[q];
+      float4 m = m4[q], pp = p4[q];
+      m.x = fmaf(momentum, m.x, g4[q].x * s);
+      m.y = fmaf(momentum, m.y, g4[q].y * s);
+      m.z = fmaf(momentum, m.z, g4[q].z * s);
+      m.w = fmaf(momentum, m.w, g4[q].w * s);
+      pp.x = fmaf(-lr, m.x, pp.x);
+      pp.y = fmaf(-lr, m.y, pp.y);
+      pp.z = fmaf(-lr, m.z, pp.z);
+      pp.w = fmaf(-lr, m.w, pp.w);
+      store4(mom + el[q], m);
+      if (kMaster) store4(ref + el[q], pp);
+      store4(param + el[q], pp);
     }
   }
+}
+
+// DEFT_SGD_UNROLL (1, 2 or 4): units per thread per pass of sgd_local_kernel
+static int sgd_unroll() {
+  static int v = [] {
+    const char* e = getenv("DEFT_SGD_UNROLL");
+    const int x = e ? atoi(e) : 2;
+    return x == 1 || x == 4 ? x : 2;
+  }();
+  return v;
+}
+// DEFT_SGD_CTAS_PER_SM: grid cap of sgd_local_kernel = 148 x this (default 8)
+static int sgd_ctas_per_sm() {
+  static int v = [] {
+    const char* e = getenv("DEFT_SGD_CTAS_PER_SM");
+    const int x = e ? atoi(e) : 8;
+    return x < 1 ? 1 : (x > 32 ? 32 : x);
+  }();
+  return v;
 }
 
 cudaError_t launch_sgd_local(const void* grad, int dtype, void* param, float* master,
@@ -596,16 +634,20 @@ cudaError_t launch_sgd_local(const void* grad, int dtype, void* param, float* ma
     }
     const int64_t total = t.first_vec[t.count];
     if (total == 0) continue;
-    int64_t grid = (total + kLocalThreads - 1) / kLocalThreads;
-    if (grid > 148 * 8) grid = 148 * 8;
-    if (dtype == 0)
-      sgd_local_kernel<float><<<(int)grid, kLocalThreads, 0, stream>>>(
-          reinterpret_cast<const float*>(grad), reinterpret_cast<float*>(param), nullptr, mom, t,
-          lr, momentum);
-    else
-      sgd_local_kernel<__nv_bfloat16><<<(int)grid, kLocalThreads, 0, stream>>>(
-          reinterpret_cast<const __nv_bfloat16*>(grad), reinterpret_cast<__nv_bfloat16*>(param),
-          master, mom, t, lr, momentum);
+    const int U = sgd_unroll();
+    int64_t grid = (total + (int64_t)kLocalThreads * U - 1) / ((int64_t)kLocalThreads * U);
+    if (grid > 148 * sgd_ctas_per_sm()) grid = 148 * sgd_ctas_per_sm();
+#define DEFT_SGD_LAUNCH(UU)                                                                      \
+  if (dtype == 0)                                                                              \
+    sgd_local_kernel<float, UU><<<(int)grid, kLocalThreads, 0, stream>>>(                      \
+        reinterpret_cast<const float*>(grad), reinterpret_cast<float*>(param), nullptr, mom, t, \
+        lr, momentum);                                                                         \
+  else                                                                                         \
+    sgd_local_kernel<__nv_bfloat16, UU><<<(int)grid, kLocalThreads, 0, stream>>>(              \
+        reinterpret_cast<const __nv_bfloat16*>(grad), reinterpret_cast<__nv_bfloat16*>(param), \
+        master, mom, t, lr, momentum);
+    if (U == 1) { DEFT_SGD_LAUNCH(1) } else if (U == 4) { DEFT_SGD_LAUNCH(4) } else { DEFT_SGD_LAUNCH(2) }
+#undef DEFT_SGD_LAUNCH
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -48,7 +48,7 @@ from .errors import DeftError, InternalInvariantError
 from .partition import PartitionConfig, element_ranges, partition_buckets, partition_by_size
 from .preserver import WalkParams, feedback_loop
 from .profiles import BucketProfile, ClusterSpec, LinkSpec, ModelProfile
-from .planner import (ExecutionPlanner, IterPlan, release_runs, start_groups,
+from .planner import (ExecutionPlanner, IterPlan, LinkQueueModel, release_runs, start_groups,
                       start_groups_timed)
 from .scheduler import (DeftScheduler, OrderScheduler, ScheduleDecision,
                         nonsequential_candidates, priority_order, sync_schedule_time_us,
@@ -112,7 +112,12 @@ class DeftConfig:
     # (all-reduce + update in one launch, no all-gather).  None = the measured
     # default (DEFT_ONESHOT_MAX_BYTES, else ONESHOT_DEFAULT_BYTES); 0 = never
     oneshot_max_bytes: int | None = None
-    defer_tail: bool = True                 # delayed schedules: last transfers -> next iteration
+    # delayed schedules under CUDA graphs (per-iteration joins): fresh transfers
+    # that would be exposed at the join start with the next iteration instead.
+    # "last" (or True): the backward's last release only; "predicted": also every
+    # release the link-queue model (planner.LinkQueueModel, profiled times)
+    # predicts would finish after the backward's end; False: none
+    defer_tail: bool | str = True
 
 
 class _Bucket:
@@ -565,7 +570,14 @@ class DeftDataParallel:
         # fresh transfers start with the next iteration (see _buckets_ready)
         self._deferred: list[tuple[int, int, tuple]] = []
         self._defer_tail = (not self.sync and self.world > 1 and self._sequential
-                            and self.cfg.defer_tail)
+                            and bool(self.cfg.defer_tail))
+        self._link_model = None
+        if self._defer_tail and self.cfg.defer_tail == "predicted":
+            self._link_model = LinkQueueModel(
+                [b.backward_us for b in part.buckets], [b.comm_fast_us for b in part.buckets],
+                [l.speed_ratio_to_fast for l in cluster.links])
+        elif self._defer_tail and self.cfg.defer_tail not in (True, "last"):
+            raise DeftError(f"unknown defer_tail {self.cfg.defer_tail!r}")
         self._planned = True
         return part
 
@@ -859,12 +871,14 @@ class DeftDataParallel:
         # start with the next iteration instead (they are needed an iteration
         # later), so the per-iteration join does not wait for them
         last = self._defer_tail and sum(self._fired) + len(bidxs) == len(self.buckets)
-        issue = (lambda link, slot, bl: self._deferred.append((link, slot, tuple(bl)))) \
-            if last else (lambda link, slot, bl: self._issue_rs(link, slot, bl, ev))
         fresh = [(link, slot, bidx) for bidx in bidxs
                  for link, slot in self._fresh_now.pop(bidx, ())]
         for link, slot, bl in release_runs(fresh):
-            issue(link, slot, bl)
+            if last or (self._link_model is not None and
+                        not self._link_model.admit(link, bl, bidxs)):
+                self._deferred.append((link, slot, tuple(bl)))
+            else:
+                self._issue_rs(link, slot, bl, ev)
         if self.placement == "bucket" and self._due_now:
             self._issue_updates(bidxs, ev)
         for bidx in bidxs:
@@ -926,6 +940,8 @@ class DeftDataParallel:
         self._due_now = it.due if self.placement != "start" else ()
         self._pending = list(self._bucket_nparams)
         self._fired = [False] * len(self.buckets)
+        if self._link_model is not None:
+            self._link_model.reset()
         self._in_step = True
         try:
             loss.backward()

@@ -228,3 +228,43 @@ def start_groups_timed(bucket_sizes: list[int], forward_us: list[float],
     if report is not None:
         report["feasible"] = feasible   # no forward wait predicted after the first group
     return groups
+
+
+class LinkQueueModel:
+    """Which of an iteration's fresh transfers the backward can hide, under
+    CUDA-graph execution (every side stream joins the compute stream at the end
+    of the iteration).  Each link is a FIFO (simulator.py:107-129) serving a
+    transfer for its profiled time (comm_fast_us x the link's speed ratio,
+    profiles.py:64-80); a bucket's transfers are released when its backward ends
+    (simulator.py:184-196: release = cumulative backward time, output side
+    first).  A release whose predicted completion lies past the backward's end
+    would be exposed at the join: with delayed updates (lag 2) it is needed an
+    iteration later at the earliest, so it is deferred to the start of the next
+    iteration (executor ``_buckets_ready``) instead of extending this one.
+
+    ``admit`` is called in release order; deferred transfers do not occupy the
+    link in this iteration's model."""
+
+    def __init__(self, backward_us: list[float], comm_fast_us: list[float],
+                 link_ratios: list[float], slack: float = 1.0):
+        self.release_us = []
+        t = 0.0
+        for b in backward_us:
+            t += b
+            self.release_us.append(t)
+        self.end_us = t
+        self.comm = [[c * r * slack for r in link_ratios] for c in comm_fast_us]
+        self.busy = [0.0] * len(link_ratios)
+
+    def reset(self):
+        self.busy = [0.0] * len(self.busy)
+
+    def admit(self, link: int, bidxs, ready: list[int]) -> bool:
+        """True: issue now (the link drains it before the backward ends); False:
+        defer.  `ready` = the buckets whose backward end released it."""
+        t = max(self.release_us[b] for b in ready)
+        done = max(self.busy[link], t) + sum(self.comm[b][link] for b in bidxs)
+        if done > self.end_us:
+            return False
+        self.busy[link] = done
+        return True

@@ -80,12 +80,13 @@ def equal_dual():
 
 
 def _config(lr, momentum, partition_size, cuda_graphs, placement, scheme, lookahead=32,
-            n_slots=6, startup_us=0, oneshot=0):
+            n_slots=6, startup_us=0, oneshot=0, defer=True):
     return D.DeftConfig(lr=lr, momentum=momentum, autocast_dtype=None,
                         partition=D.PartitionConfig(partition_size=partition_size,
                                                     comm_startup_us=startup_us),
                         cuda_graphs=cuda_graphs, update_placement=placement, scheme=scheme,
-                        lookahead=lookahead, n_slots=n_slots, oneshot_max_bytes=oneshot)
+                        lookahead=lookahead, n_slots=n_slots, oneshot_max_bytes=oneshot,
+                        defer_tail=defer)
 
 
 def _xs_for(ddp, model, flat):
@@ -107,14 +108,14 @@ def theta0_for(total, dtype):
 def run_executor(world, rank, iterations, n_buckets=48, total=48_000, lr=0.05, momentum=0.9,
                  dtype=torch.float32, comm_us=900, group=None, cuda_graphs=True,
                  x_fn=flat_x, placement="end", scheme="deft", partition_size=10**9,
-                 model_cls=None, startup_us=0, hw_probe=False, oneshot=0):
+                 model_cls=None, startup_us=0, hw_probe=False, oneshot=0, defer=True):
     """One rank of a real (one process per GPU) run on the probe.  Returns
     (master fp32 CPU -- the parameters for fp32 models --, params CPU in the
     model dtype, theta0, decisions as dicts, bucket ranges).  ``hw_probe``: the
     non-sequential scheme scores its candidates by timing them on the GPU."""
     model = (model_cls or Probe)(probe_sizes(total)).cuda().to(dtype)
     cfg = _config(lr, momentum, partition_size, cuda_graphs, placement, scheme,
-                  startup_us=startup_us, oneshot=oneshot)
+                  startup_us=startup_us, oneshot=oneshot, defer=defer)
     ddp = D.DeftDataParallel(model, cfg, process_group=group)
     prof = uniform_profile(n_buckets, total // n_buckets, comm_us=comm_us)
     probe = None
@@ -138,7 +139,7 @@ def run_executor(world, rank, iterations, n_buckets=48, total=48_000, lr=0.05, m
 def run_loopback(world, iterations, n_buckets=48, total=48_000, lr=0.05, momentum=0.9,
                  dtype=torch.float32, comm_us=900, cuda_graphs=True, x_fn=flat_x,
                  placement="end", scheme="deft", partition_size=10**9, model_cls=None,
-                 profile=None, cluster=None, startup_us=0, oneshot=0):
+                 profile=None, cluster=None, startup_us=0, oneshot=0, defer=True):
     """W ranks in this process on cuda:current (loopback.py), driven round-robin
     from this thread.  Returns per-rank (master, params) lists, theta0 and the
     (identical) decision stream of rank 0."""
@@ -148,7 +149,7 @@ def run_loopback(world, iterations, n_buckets=48, total=48_000, lr=0.05, momentu
     for r in range(world):
         model = (model_cls or Probe)(probe_sizes(total)).cuda().to(dtype)
         cfg = _config(lr, momentum, partition_size, cuda_graphs, placement, scheme,
-                      lookahead=look, startup_us=startup_us, oneshot=oneshot)
+                      lookahead=look, startup_us=startup_us, oneshot=oneshot, defer=defer)
         models.append(model)
         execs.append(D.DeftDataParallel(model, cfg, process_group=lbw.rank(r)))
     prof = profile or uniform_profile(n_buckets, total // n_buckets, comm_us=comm_us)

@@ -279,3 +279,13 @@ def test_loopback_collective_kernels(world, dtype):
 
 def test_kernels_run_concurrently():
     assert S.D.LoopbackWorld(2).kernels_run_concurrently()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("defer", ["predicted", False])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_loopback_deferral_policies(world, defer, dtype):
+    """Which fresh transfers move into the next iteration's graph must not change
+    the trajectory: the link-queue model (comm 900 us per bucket against 150 us
+    of backward each) defers most of them, False none."""
+    _check(world, 14, dtype=dtype, placement="start", cuda_graphs=True, defer=defer)

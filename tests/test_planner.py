@@ -219,3 +219,20 @@ def test_start_groups_timed():
     # launch cap honoured
     assert len(start_groups_timed(sizes, fwd, 10.0, 5.0, 3)) <= 3
     assert start_groups_timed([], [], 1e-3, 5.0, 8) == []
+
+
+def test_link_queue_model():
+    """Deferral model: releases at cumulative backward times 10, 20, 30, 40 us;
+    a transfer is admitted only if its link drains it by the backward's end."""
+    from paper_2503_16815_b200.planner import LinkQueueModel
+    m = LinkQueueModel([10, 10, 10, 10], [5, 25, 5, 5], [1.0, 2.0])
+    assert m.end_us == 40
+    assert m.admit(0, [0], [0])            # 10 + 5 = 15
+    assert not m.admit(0, [1], [1])        # 20 + 25 = 45 > 40: deferred, link stays at 15
+    assert m.admit(0, [2], [2])            # 30 + 5 = 35
+    assert not m.admit(0, [3], [3])        # 40 + 5 > 40 (the tail)
+    assert m.admit(1, [0], [0])            # slow link: 10 + 10 = 20
+    assert m.admit(1, [2], [1, 2])         # released at 30 (the later bucket): 40 <= 40
+    assert not m.admit(1, [3], [3])        # 40 + 10 > 40
+    m.reset()
+    assert m.busy == [0.0, 0.0] and m.admit(0, [1], [0])   # 10 + 25 = 35

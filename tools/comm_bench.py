@@ -104,8 +104,8 @@ def main():
     W, rank = dist.get_world_size(), dist.get_rank()
     if args.nvml:
         nvml_init(dev)
-    sizes = [int(x) for x in args.sizes_mb.split(",")]
-    max_elems = max(sizes) * 2**20 // 4
+    sizes = [float(x) for x in args.sizes_mb.split(",")]
+    max_elems = int(max(sizes) * 2**20) // 4
     comm = BucketComm(rank, W, 1, max_elems, torch.float32, dev)
     comm.grads.normal_()
     comm.set_update_blocks(args.update_blocks)
@@ -113,7 +113,7 @@ def main():
     s = torch.cuda.Stream(dev)
     rows = []
     for mb in sizes:
-        n = mb * 2**20 // 4
+        n = int(mb * 2**20) // 4
         nbytes = n * 4
         res = {"bucket_mb": mb, "world": W}
         if args.check:
