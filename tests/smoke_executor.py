@@ -316,11 +316,15 @@ def run_smoke_executor(iterations=12):
     return err
 
 
-def run_smoke_loopback(world=4, iterations=10, dtype=torch.float32, placement="start"):
+def run_smoke_loopback(world=4, iterations=10, dtype=torch.float32, placement="start",
+                       oneshot=0, partition_size=10**9):
     """W ranks on this GPU: reduce-scatter (SM + copy-engine channels), fused
-    update + parameter all-gather, barriers -- against the oracle."""
+    update + parameter all-gather, barriers (and, with ``oneshot``, the one-shot
+    all-reduce + update for buckets of at most that many bytes) -- against the
+    oracle."""
     masters, params, theta0, decisions, buckets, _ = run_loopback(
-        world, iterations, dtype=dtype, placement=placement)
+        world, iterations, dtype=dtype, placement=placement, oneshot=oneshot,
+        partition_size=partition_size)
     for r in range(1, world):
         assert decisions[r] == decisions[0], "ranks planned different streams"
     want_m, want_p = oracle_theta(theta0, decisions[0], world, iterations, dtype=dtype)
