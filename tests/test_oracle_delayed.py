@@ -52,3 +52,35 @@ def test_probe_gradient_is_exact():
         model(xs).backward()
         for p, x in zip(model.ps, xs):
             assert torch.equal(p.grad, (x * p.detach()).to(dtype))
+
+
+@pytest.mark.parametrize("world", [1, 4])
+@pytest.mark.parametrize("lag", [1, 2])
+@pytest.mark.parametrize("foreach", [False, True])
+def test_oracle_is_torch_optim_sgd(decisions, world, lag, foreach):
+    """Pins the oracle's update arithmetic to a library implementation: the same
+    delayed group gradients fed to torch.optim.SGD(momentum=0.9, dampening 0) --
+    one .step() per update event, p.grad = the k*W mean of the group -- give
+    theta bit for bit (the reference fixes only WHICH gradients form a group and
+    WHEN it applies, scheduler.py:56-61, 223-233; preserver.py:93-94)."""
+    total, iters, lr, m = 48_000, 14, 0.05, 0.9
+    th0 = S.theta0_for(total, torch.float32)
+    grad_of = lambda th, r, t: S.flat_x(total, r, t) * th   # noqa: E731
+    want = delayed_sgd.run(th0, grad_of, decisions, world, lr, m, iters, lag=lag)
+    p = torch.nn.Parameter(th0.clone())
+    opt = torch.optim.SGD([p], lr=lr, momentum=m, foreach=foreach)
+    events = delayed_sgd.events_by_iteration(decisions)
+    summed = {}
+    for s in range(iters + 1):
+        for origins, k in events.get(s - lag, ()):
+            g = torch.zeros_like(th0)
+            for o in origins:
+                g += summed.pop(o)
+            g /= world * k
+            p.grad = g
+            opt.step()
+        if s == iters:
+            break
+        with torch.no_grad():
+            summed[s] = sum(grad_of(p.detach(), r, s) for r in range(world))
+    assert torch.equal(p.detach(), want)
