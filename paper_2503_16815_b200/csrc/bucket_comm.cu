@@ -26,6 +26,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <vector>
 
@@ -604,11 +605,14 @@ static int sgd_unroll() {
   }();
   return v;
 }
-// DEFT_SGD_CTAS_PER_SM: grid cap of sgd_local_kernel = 148 x this (default 8)
+// DEFT_SGD_CTAS_PER_SM: grid cap of sgd_local_kernel = 148 x this (default 16:
+// two waves of 8 resident CTAs per SM; tools/update_bench.py on ResNet-101's
+// 44.5 M parameters: 2 x 16 -> 0.974 of the HBM peak, 1 x 8 -> 0.946,
+// profiles/r02_update_w1.jsonl)
 static int sgd_ctas_per_sm() {
   static int v = [] {
     const char* e = getenv("DEFT_SGD_CTAS_PER_SM");
-    const int x = e ? atoi(e) : 8;
+    const int x = e ? atoi(e) : 16;
     return x < 1 ? 1 : (x > 32 ? 32 : x);
   }();
   return v;
@@ -1182,7 +1186,13 @@ namespace deft {
 // "start" placement uses still streams at NVLink rate.
 // ============================================================================
 constexpr int kUpdTmaThreads = 256;
-constexpr int kUpdTmaStagesDefault = 3;   // DEFT_UPDATE_TMA_STAGES: 3 or 6
+// ring of S shared-memory stages of which up to P hold chunks whose bulk stores
+// are still reading them (DEFT_UPDATE_TMA_PIPE=S:P, 3:0 | 4:1 | 6:2): loads run
+// S - 1 - P chunks ahead, and refilling a stage waits only for the stores of
+// the chunk P + 1 back -- never for the chunk just stored (whose remote stores
+// drain at NVLink latency)
+constexpr int kUpdTmaStagesDefault = 4;
+constexpr int kUpdTmaPendingDefault = 1;
 constexpr int kUpdChunk = 2048;  // elements per chunk (multiple of 8)
 
 __device__ __forceinline__ void tma_store_1d(void* dst_gmem, const void* src_smem,
@@ -1194,15 +1204,16 @@ __device__ __forceinline__ void tma_store_1d(void* dst_gmem, const void* src_sme
 __device__ __forceinline__ void tma_store_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ void tma_store_wait_read_all() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+template <int N>
+__device__ __forceinline__ void tma_store_wait_read() {   // all but the newest N groups
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void tma_store_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 
-template <typename T, int W, int kUpdTmaStages, bool kLoop = false>
+template <typename T, int W, int kUpdTmaStages, int kPending, bool kLoop = false>
 __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
     PeerPtrs P, int rank_arg, int64_t slot_base, const __grid_constant__ ChunkTable t_arg,
     float lr, float momentum, float scale, float* __restrict__ mom_arg,
@@ -1259,11 +1270,15 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
     table_chunk(t, kUpdChunk, c, e0, len);
   };
   auto base = [&](int st) { return usmem + (size_t)st * kStage; };
+  static_assert(kPending >= 0 && kPending <= kUpdTmaStages - 2, "ring too small");
+  constexpr int kAhead = kUpdTmaStages - 1 - kPending;   // loads in flight
   auto issue_load = [&](int64_t c) {
     const int st = (int)((c - c_begin) % kUpdTmaStages);
     int64_t e0, len;
     chunk_range(c, &e0, &len);
-    tma_store_wait_read_all();  // earlier stores no longer read this stage
+    // the stage's previous chunk (c - S) was stored kPending + 1 chunks ago:
+    // only its bulk stores must have finished reading it
+    tma_store_wait_read<kPending>();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     const uint32_t bg = (uint32_t)(len * sizeof(T)), bf = (uint32_t)(len * 4);
     mbar_expect_tx(&full[st], bg + 2 * bf);
@@ -1272,11 +1287,11 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
     tma_load_1d(base(st) + kG + kF, ref + e0, bf, &full[st]);
   };
   if (threadIdx.x == 0)
-    for (int64_t c = c_begin; c < min(c_end, c_begin + kUpdTmaStages - 1); ++c) issue_load(c);
+    for (int64_t c = c_begin; c < min(c_end, c_begin + kAhead); ++c) issue_load(c);
   for (int64_t c = c_begin; c < c_end; ++c) {
     const int st = (int)((c - c_begin) % kUpdTmaStages);
     const uint32_t parity = (uint32_t)(((c - c_begin) / kUpdTmaStages) & 1);
-    if (threadIdx.x == 0 && c + kUpdTmaStages - 1 < c_end) issue_load(c + kUpdTmaStages - 1);
+    if (threadIdx.x == 0 && c + kAhead < c_end) issue_load(c + kAhead);
     mbar_wait(&full[st], parity);
     int64_t e0, len;
     chunk_range(c, &e0, &len);
@@ -1324,10 +1339,13 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
   peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 2u);
 }
 
-static int upd_tma_stages() {
+// DEFT_UPDATE_TMA_PIPE=S:P -> 30 (3:0), 41 (4:1, default) or 62 (6:2)
+static int upd_tma_pipe() {
   static int v = [] {
-    const char* e = getenv("DEFT_UPDATE_TMA_STAGES");
-    return e && atoi(e) == 6 ? 6 : kUpdTmaStagesDefault;
+    const char* e = getenv("DEFT_UPDATE_TMA_PIPE");
+    if (!e) return kUpdTmaStagesDefault * 10 + kUpdTmaPendingDefault;
+    const int x = atoi(e) * 10 + (strchr(e, ':') ? atoi(strchr(e, ':') + 1) : 0);
+    return x == 30 || x == 41 || x == 62 ? x : kUpdTmaStagesDefault * 10 + kUpdTmaPendingDefault;
   }();
   return v;
 }
@@ -1352,24 +1370,23 @@ bool launch_update_allgather_tma(const PeerPtrs& P, int rank, int world, int dty
     if (max_blocks > 0 && grid > max_blocks) grid = max_blocks;
     grid = cap_grid(P, grid);
     const size_t esz = dtype == 0 ? 4 : 2;
-    const int stages = upd_tma_stages();
-    const size_t smem = (size_t)stages *
+    const int pipe = upd_tma_pipe();
+    const size_t smem = (size_t)(pipe / 10) *
                         (kUpdChunk * esz + 2 * kUpdChunk * 4 + (dtype == 0 ? 0 : kUpdChunk * esz));
-#define DEFT_UPT_LAUNCH(TT, WW, SS)                                                            \
+#define DEFT_UPT_LAUNCH(TT, WW, SS, PP)                                                        \
   {                                                                                            \
-    cudaFuncSetAttribute(update_allgather_tma_kernel<TT, WW, SS>,                              \
+    cudaFuncSetAttribute(update_allgather_tma_kernel<TT, WW, SS, PP>,                          \
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
-    update_allgather_tma_kernel<TT, WW, SS><<<grid, kUpdTmaThreads, smem, stream>>>(           \
+    update_allgather_tma_kernel<TT, WW, SS, PP><<<grid, kUpdTmaThreads, smem, stream>>>(       \
         P, rank, slot_base, t, lr, momentum, grad_scale, mom, nullptr);                        \
   }
+#define DEFT_UPT_PIPE(TT, WW)                                                                  \
+  if (pipe == 30) DEFT_UPT_LAUNCH(TT, WW, 3, 0)                                                \
+  else if (pipe == 62) DEFT_UPT_LAUNCH(TT, WW, 6, 2)                                           \
+  else DEFT_UPT_LAUNCH(TT, WW, 4, 1)
 #define DEFT_UPT_CASE(WW)                                                                      \
   case WW:                                                                                     \
-    if (dtype == 0) {                                                                          \
-      if (stages == 6) DEFT_UPT_LAUNCH(float, WW, 6) else DEFT_UPT_LAUNCH(float, WW, 3)        \
-    } else {                                                                                   \
-      if (stages == 6) DEFT_UPT_LAUNCH(__nv_bfloat16, WW, 6)                                   \
-      else DEFT_UPT_LAUNCH(__nv_bfloat16, WW, 3)                                               \
-    }                                                                                          \
+    if (dtype == 0) { DEFT_UPT_PIPE(float, WW) } else { DEFT_UPT_PIPE(__nv_bfloat16, WW) }     \
     break;
     switch (world) {
       DEFT_UPT_CASE(2) DEFT_UPT_CASE(3) DEFT_UPT_CASE(4) DEFT_UPT_CASE(5)
@@ -1377,6 +1394,7 @@ bool launch_update_allgather_tma(const PeerPtrs& P, int rank, int world, int dty
       default: break;
     }
 #undef DEFT_UPT_CASE
+#undef DEFT_UPT_PIPE
 #undef DEFT_UPT_LAUNCH
     count_launch();
   }
@@ -1479,9 +1497,10 @@ cudaError_t launch_update_tma_loopback(const PeerPtrs& P, int world, int dtype,
                         (kUpdChunk * esz + 2 * kUpdChunk * 4 + (dtype == 0 ? 0 : kUpdChunk * esz));
 #define DEFT_UPL_LAUNCH(TT, WW)                                                               \
   {                                                                                           \
-    cudaFuncSetAttribute(update_allgather_tma_kernel<TT, WW, kUpdTmaStagesDefault, true>,     \
+    cudaFuncSetAttribute(update_allgather_tma_kernel<TT, WW, kUpdTmaStagesDefault,            \
+                                                     kUpdTmaPendingDefault, true>,            \
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
-    update_allgather_tma_kernel<TT, WW, kUpdTmaStagesDefault, true>                           \
+    update_allgather_tma_kernel<TT, WW, kUpdTmaStagesDefault, kUpdTmaPendingDefault, true>    \
         <<<dim3(grid, world), kUpdTmaThreads, smem, stream>>>(P, 0, slot_base, h[0].t, lr,    \
                                                               momentum, grad_scale, nullptr,  \
                                                               d);                             \

@@ -37,19 +37,35 @@ NVML = {}
 
 
 def nvlink_bytes():
-    """(tx, rx) NVLink data bytes of this GPU so far (NVML counters, KiB units)."""
+    """{family: (tx, rx)} NVLink bytes of this GPU so far, from every NVML counter
+    family this driver offers (summed over links): COUNT_XMIT/RCV_BYTES (the
+    per-link byte counters) and THROUGHPUT_DATA_TX/RX (KiB units)."""
     h = NVML.get("h")
     if h is None:
         return None
     import pynvml as N
-    fields = []
-    for link in range(NVML["links"]):
-        fields += [(N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, link),
-                   (N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, link)]
-    vals = N.nvmlDeviceGetFieldValues(h, fields)
-    tx = sum(v.value.ullVal for v in vals[0::2] if v.nvmlReturn == 0)
-    rx = sum(v.value.ullVal for v in vals[1::2] if v.nvmlReturn == 0)
-    return tx * 1024, rx * 1024
+    fams = {"count_bytes": (N.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES,
+                            N.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES, 1),
+            "throughput_data": (N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 1024)}
+    out = {}
+    for fam, (ftx, frx, unit) in fams.items():
+        fields = []
+        for link in range(NVML["links"]):
+            fields += [(ftx, link), (frx, link)]
+        try:
+            vals = N.nvmlDeviceGetFieldValues(h, fields)
+        except Exception as e:  # noqa: BLE001
+            out[fam] = repr(e)
+            continue
+        ok = [v for v in vals if v.nvmlReturn == 0]
+        if not ok:
+            out[fam] = f"nvmlReturn {vals[0].nvmlReturn}"
+            continue
+        tx = sum(v.value.ullVal for v in vals[0::2] if v.nvmlReturn == 0)
+        rx = sum(v.value.ullVal for v in vals[1::2] if v.nvmlReturn == 0)
+        out[fam] = (tx * unit, rx * unit)
+    return out
 
 
 def nvml_init(device):
@@ -63,27 +79,46 @@ def nvml_init(device):
         NVML["error"] = repr(e)
 
 
-def timeit(fn, reps, warm, stream, device, nv=None, key=None):
+def timeit(fn, reps, warm, stream, device):
+    """ms per call, CUDA events on `stream`, after a barrier, max over ranks."""
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
     dist.barrier()
-    before = nvlink_bytes() if nv is not None else None
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
     for _ in range(reps):
         fn()
     b.record(stream)
     torch.cuda.synchronize()
-    if before is not None:
-        import time
-        time.sleep(0.15)          # counters are sampled by the driver
-        after = nvlink_bytes()
-        nv[key] = {"tx_per_launch": (after[0] - before[0]) / reps,
-                   "rx_per_launch": (after[1] - before[1]) / reps}
     t = torch.tensor([a.elapsed_time(b) / reps], device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def nvml_count(fn, reps, nv, key):
+    """NVLink bytes per call of `fn` (NVML counters read before and after `reps`
+    barrier-aligned calls; never inside a timed region -- reading NVML takes
+    milliseconds and would skew the ranks)."""
+    import time
+    torch.cuda.synchronize()
+    dist.barrier()
+    time.sleep(0.2)
+    before = nvlink_bytes()
+    dist.barrier()
+    for _ in range(reps):
+        fn()
+    torch.cuda.synchronize()
+    dist.barrier()
+    time.sleep(0.2)          # counters are sampled by the driver
+    after = nvlink_bytes()
+    res = {}
+    for fam, v in after.items():
+        if isinstance(v, tuple) and isinstance(before.get(fam), tuple):
+            res[fam] = {"tx": (v[0] - before[fam][0]) / reps, "rx": (v[1] - before[fam][1]) / reps}
+        else:
+            res[fam] = v
+    nv[key] = res
 
 
 def main():
@@ -134,17 +169,18 @@ def main():
                 dist.barrier()
         nv = {} if args.nvml else None
         with torch.cuda.stream(s):
-            res["rs_sm_ms"] = timeit(lambda: comm.reduce_scatter(_native.CHANNEL_SM, 0, 0, n, s),
-                                     args.reps, 3, s, dev, nv, "rs_sm")
-            res["rs_ce_ms"] = timeit(lambda: comm.reduce_scatter(_native.CHANNEL_CE, 0, 0, n, s),
-                                     args.reps, 3, s, dev, nv, "rs_ce")
-            # the multi-bucket entry point: the TMA-pipelined update kernel
-            res["upd_ag_ms"] = timeit(
-                lambda: comm.update_multi(0, [(0, n)], 1e-3, 1e-9, 0.9, mom, s),
-                args.reps, 3, s, dev, nv, "upd_ag")
-            res["oneshot_ms"] = timeit(
-                lambda: comm.sync_update_multi(0, [(0, n)], 1e-3, 1e-9, 0.9, mom, s),
-                args.reps, 3, s, dev, nv, "oneshot")
+            kernels = {
+                "rs_sm": lambda: comm.reduce_scatter(_native.CHANNEL_SM, 0, 0, n, s),
+                "rs_ce": lambda: comm.reduce_scatter(_native.CHANNEL_CE, 0, 0, n, s),
+                # the multi-bucket entry point: the TMA-pipelined update kernel
+                "upd_ag": lambda: comm.update_multi(0, [(0, n)], 1e-3, 1e-9, 0.9, mom, s),
+                "oneshot": lambda: comm.sync_update_multi(0, [(0, n)], 1e-3, 1e-9, 0.9, mom, s),
+            }
+            for key, fn in kernels.items():
+                res[f"{key}_ms"] = timeit(fn, args.reps, 3, s, dev)
+            if nv is not None:
+                for key, fn in kernels.items():
+                    nvml_count(fn, args.reps, nv, key)
 
             def deft():
                 comm.reduce_scatter(_native.CHANNEL_SM, 0, 0, n, s)
@@ -154,8 +190,9 @@ def main():
                 x = torch.randn(n, device=dev)
                 p = torch.randn(n, device=dev)
                 v = torch.zeros(n, device=dev)
-                res["nccl_ar_ms"] = timeit(lambda: dist.all_reduce(x), args.reps, 3, s, dev,
-                                           nv, "nccl_ar")
+                res["nccl_ar_ms"] = timeit(lambda: dist.all_reduce(x), args.reps, 3, s, dev)
+                if nv is not None:
+                    nvml_count(lambda: dist.all_reduce(x), args.reps, nv, "nccl_ar")
 
                 def nccl_sgd():
                     dist.all_reduce(x)
@@ -176,8 +213,7 @@ def main():
         if nv is not None:
             # algorithmic NVLink bytes per rank: RS rx (W-1)/W, AG tx (W-1)/W,
             # one-shot rx (W-1) x bucket; the measured counters beside them
-            res["nvlink"] = {k: {"tx": int(v["tx_per_launch"]), "rx": int(v["rx_per_launch"])}
-                             for k, v in nv.items()}
+            res["nvlink"] = nv
             res["nvlink_algorithmic"] = {"rs_rx": int(frac * nbytes), "upd_ag_tx":
                                          int(frac * nbytes), "oneshot_rx": (W - 1) * nbytes}
         if NVML.get("error"):
