@@ -22,8 +22,9 @@ What the fields mean on hardware (``RunReport.from_measurement``):
 Sweep axes: ``partition_size`` re-partitions the real buckets; ``bandwidth_scale``
 scales the PLANNED communication times (the schedule DeFT computes), the
 links themselves run at NVLink speed; ``gpu_count`` points other than the
-launched world size are skipped.  ``nonsequential`` is the simulator-scored
-search baseline (scheduler.py:421-472) and is not run.
+launched world size are skipped.  ``nonsequential`` (scheduler.py:421-472)
+runs its candidate search on the executor: the four candidates are scored by
+a timed hardware probe on this batch instead of ``simulate()``.
 """
 from __future__ import annotations
 
@@ -40,7 +41,7 @@ from .preserver import WalkParams, check_sequence, extract_batch_sequence
 from .profiles import ClusterSpec, ModelProfile
 from .scheduler import SCHEMES, Schedule
 
-HW_SCHEMES = ("wfbp", "priority", "deft", "deft_single_link")
+HW_SCHEMES = ("wfbp", "priority", "nonsequential", "deft", "deft_single_link")
 
 
 # ----------------------------------------------------------------- config (cli.py:52-175)
@@ -470,7 +471,9 @@ def run_hw_experiment(cfg: ExperimentConfig, make_model: Callable, batch, loss_f
             model, ddp = executor(scheme, p_partition)
             links = (ClusterSpec(links=(cluster.fast_link,))
                      if scheme == "deft_single_link" else cluster)
-            part = ddp.plan(p_profile, links)
+            # nonsequential: the candidates are timed on this hardware, not simulated
+            probe = (batch, loss_fn) if scheme == "nonsequential" else None
+            part = ddp.plan(p_profile, links, probe=probe)
             ddp.warm_up(batch, loss_fn, min_steps=warmup)
             u0 = ddp.updates_applied
             total_ms = timed_steps(ddp, model, cfg.iterations)
