@@ -605,15 +605,16 @@ static int sgd_unroll() {
   }();
   return v;
 }
-// DEFT_SGD_CTAS_PER_SM: grid cap of sgd_local_kernel = 148 x this (default 16:
-// two waves of 8 resident CTAs per SM; tools/update_bench.py on ResNet-101's
-// 44.5 M parameters: 2 x 16 -> 0.974 of the HBM peak, 1 x 8 -> 0.946,
-// profiles/r02_update_w1.jsonl)
+// DEFT_SGD_CTAS_PER_SM: grid cap of sgd_local_kernel = 148 x this (default 32:
+// four waves of 8 resident CTAs per SM, each CTA a short grid-stride loop;
+// tools/update_bench.py on ResNet-101's 44.5 M parameters, unroll 2: 32 -> 0.998
+// of the HBM peak, 16 -> 0.968-0.974, 8 -> 0.945; unroll 1 x 8 (round 1) -> 0.946;
+// profiles/r02_update_w1*.jsonl)
 static int sgd_ctas_per_sm() {
   static int v = [] {
     const char* e = getenv("DEFT_SGD_CTAS_PER_SM");
-    const int x = e ? atoi(e) : 16;
-    return x < 1 ? 1 : (x > 32 ? 32 : x);
+    const int x = e ? atoi(e) : 32;
+    return x < 1 ? 1 : (x > 64 ? 64 : x);
   }();
   return v;
 }
