@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--start-grouping", default="auto", choices=["auto", "size", "timed"],
                     help="how start-placement updates are grouped into launches")
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs")
+    ap.add_argument("--oneshot-mb", type=float, default=None,
+                    help="buckets of at most this many MB of gradients sync one-shot "
+                         "(DeftConfig.oneshot_max_bytes; default: the executor's)")
     ap.add_argument("--defer", default="last", choices=["last", "predicted", "none"],
                     help="graph mode: which fresh transfers start with the next iteration "
                          "(DeftConfig.defer_tail)")
@@ -629,6 +632,8 @@ def main():
                        update_blocks=args.update_blocks, scheme=args.scheme,
                        start_grouping=args.start_grouping,
                        defer_tail=False if args.defer == "none" else args.defer,
+                       oneshot_max_bytes=None if args.oneshot_mb is None else
+                       int(args.oneshot_mb * 2**20),
                        autocast_dtype=None if args.model == "gpt2" else torch.bfloat16,
                        partition=D.PartitionConfig(partition_size=psize, mu=1.0))
     ddp = D.DeftDataParallel(model, cfg)
@@ -808,6 +813,7 @@ def main():
                                                for d in pair for u in d.update_events}),
                        "cuda_graphs": ddp.cfg.cuda_graphs, "graph_choice": ddp.graph_choice,
                        "graphs_captured": len(ddp._graphs),
+                       "oneshot_buckets": sum(ddp._oneshot), "defer_tail": ddp.cfg.defer_tail,
                        "warmup_steps_run": warm, "setup_s": round(t_setup, 2)},
             "e2e": {"value": round(e2e_value, 2), "unit": "samples/s",
                     "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": 4,
