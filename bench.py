@@ -31,6 +31,11 @@ if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
 
 BATCH = 64
 METRIC = "samples/sec (DeFT delayed-update DP training step)"
+# The convergence walk the update-frequency controller is driven by: the values the
+# reference ships for its merged-update experiments (pkg/fixtures/
+# walk_merged_updates.json = experiment_vgg.json:18-25).  --walk FILE overrides.
+DEFAULT_WALK = {"s0": 0.2103, "s_star": 0.0, "eta": 0.01, "mu_t": 0.851934758267416,
+                "sigma_t": 181.21080499210186, "epsilon": 0.01}
 
 
 def parse():
@@ -54,6 +59,9 @@ def parse():
     ap.add_argument("--start-grouping", default="auto", choices=["auto", "size", "timed"],
                     help="how start-placement updates are grouped into launches")
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs")
+    ap.add_argument("--walk", default=None,
+                    help="JSON file of the convergence walk (preserver.WalkParams fields); "
+                         "default: the reference's walk_merged_updates values")
     ap.add_argument("--oneshot-mb", type=float, default=None,
                     help="buckets of at most this many MB of gradients sync one-shot "
                          "(DeftConfig.oneshot_max_bytes; default: the executor's)")
@@ -151,6 +159,7 @@ class ClockSampler:
         self.rows = []
         self.proc = None
         self.window = None
+        self.load = [time.monotonic(), None]
 
     def mark(self, start: bool):
         """Open / close the timed region; summary() reports the samples inside."""
@@ -158,6 +167,12 @@ class ClockSampler:
             self.window = [time.monotonic(), None]
         else:
             self.window[1] = time.monotonic()
+
+    def end_load(self):
+        """Close the load window (opened by __enter__, before the warm-up): the
+        throttle reasons are taken over all of it, so they cover >= 1 s of load
+        even when the timed region itself is shorter."""
+        self.load[1] = time.monotonic()
 
     def __enter__(self):
         try:
@@ -185,18 +200,30 @@ class ClockSampler:
         win = None
         if self.window and self.window[1] is not None:
             win = [r[1:] for r in self.rows if self.window[0] <= r[0] <= self.window[1]]
+        lo, hi = self.load[0], self.load[1] or time.monotonic()
+        load = [r[1:] for r in self.rows if lo <= r[0] <= hi]
         use = win if win else rows
         if not use:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(r[0]) for r in use if r[0].replace(".", "").isdigit())
+
+        def med(rs):
+            sm = sorted(float(r[0]) for r in rs if r[0].replace(".", "").isdigit())
+            return sm[len(sm) // 2] if sm else None
         mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in use for n, v in zip(names, r[2:6]) if v == "Active"})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+        # reasons: the timed region AND the whole load window around it
+        reasons = sorted({n for r in use + load for n, v in zip(names, r[2:6])
+                          if v == "Active"})
+        return {"sm_mhz": med(use), "sm_max_mhz": mx,
                 "reasons": reasons, "samples": len(use),
                 "samples_all": len(rows), "period_ms": self.period_ms,
                 "window": "timed region" if win else "whole run (no sample in the timed region)",
-                "window_s": round(self.window[1] - self.window[0], 3) if win else None}
+                "window_s": round(self.window[1] - self.window[0], 3) if win else None,
+                "load_window": "warm-up start to end of the last timed region",
+                "load_window_s": round(hi - lo, 3), "load_samples": len(load),
+                "load_sm_mhz": med(load),
+                "load_sm_min_mhz": min((float(r[0]) for r in load
+                                        if r[0].replace(".", "").isdigit()), default=None)}
 
 
 # ----------------------------------------------------------------- CPU path
@@ -557,6 +584,7 @@ def ddp_baseline(args, world, rank, device, dist):
     b.record()
     torch.cuda.synchronize()
     clk.mark(False)
+    clk.end_load()
     ms = a.elapsed_time(b)
     if world > 1:
         t = torch.tensor([ms], device=device)
@@ -624,7 +652,7 @@ def main():
 
     # 2) DeFT: profile on this GPU, plan (partition + feedback loop), run
     walk = D.WalkParams.from_dict(
-        json.loads((ROOT / "tests" / "golden" / "inputs.json").read_text())["walk"])
+        json.loads(Path(args.walk).read_text()) if args.walk else DEFAULT_WALK)
     psize = 6_500_000 if args.bucket_mb is None else int(args.bucket_mb * 2**20 / 4)
     cfg = D.DeftConfig(lr=0.1, momentum=0.9, walk=walk,
                        cuda_graphs=False if args.eager else "auto",
@@ -724,6 +752,7 @@ def main():
     for _ in range(2):
         e2e_step()
     ms_e2e = timed(e2e_step, args.steps)
+    clk.end_load()
     e2e_value = args.batch * world * args.steps / (ms_e2e / 1e3)
     h2d_bytes = hx.numel() * hx.element_size() + hy.numel() * hy.element_size()
 
