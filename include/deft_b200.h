@@ -147,6 +147,13 @@ deft_status_t deft_comm_set_update_blocks(deft_comm* c, int32_t blocks);
  * instead of hanging the GPU.  A negative argument keeps the current value.
  * Both must be equal on every rank. */
 deft_status_t deft_comm_configure(deft_comm* c, int32_t grid_cap, int64_t spin_timeout_ms);
+/* Diagnostics (no reference counterpart): dev_stamps (device, >= 256 x 8
+ * uint64, or NULL to stop) receives globaltimer ns stamps of every block of the
+ * TMA reduce-scatter, TMA update + all-gather and one-shot kernels at their
+ * phase boundaries [block * 8 + k]: 0 start, 1 epoch read, 2 entry barrier
+ * passed, 3 first stage landed, 4 body done, 5 stores drained, 6 end.  Phases a
+ * kernel does not have stay untouched.  tools/comm_bench.py --phases. */
+deft_status_t deft_comm_set_phase_trace(deft_comm* c, uint64_t* dev_stamps);
 
 /* grad_dtype codes */
 #define DEFT_DTYPE_F32 0

@@ -25,7 +25,7 @@ EXPORTED = (
     "deft_sched_carry_bytes",
     "deft_mem_alloc", "deft_mem_free", "deft_mem_open", "deft_mem_close",
     "deft_comm_flag_bytes", "deft_comm_create", "deft_comm_destroy",
-    "deft_comm_set_update_blocks", "deft_comm_configure",
+    "deft_comm_set_update_blocks", "deft_comm_configure", "deft_comm_set_phase_trace",
     "deft_bucket_reduce_scatter", "deft_bucket_reduce_scatter_multi", "deft_bucket_update",
     "deft_bucket_update_multi",
     "deft_sgd_momentum_update", "deft_sgd_momentum_update_multi", "deft_gather_segments",
@@ -76,6 +76,7 @@ def _declare(lib):
         "deft_comm_destroy": (c_i32, [c_vp]),
         "deft_comm_set_update_blocks": (c_i32, [c_vp, c_i32]),
         "deft_comm_configure": (c_i32, [c_vp, c_i32, c_i64]),
+        "deft_comm_set_phase_trace": (c_i32, [c_vp, c_vp]),
         "deft_bucket_sync_update_multi": (c_i32, [c_vp, c_i32, c_i32, P(c_i64), P(c_i64),
                                                   c_f32, c_f32, c_f32, c_vp, c_vp]),
         "deft_stream_create": (c_i32, [c_i32, P(c_vp)]),

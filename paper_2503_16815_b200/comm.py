@@ -120,6 +120,13 @@ class BucketComm:
         check(_native.lib().deft_comm_configure(self._h, int(grid_cap), int(spin_timeout_ms)),
               "deft_comm_configure")
 
+    def set_phase_trace(self, stamps) -> None:
+        """Diagnostics: a device uint64 tensor (>= 256 x 8) that the TMA reduce-
+        scatter / update and one-shot kernels stamp with globaltimer ns at their
+        phase boundaries (deft_comm_set_phase_trace), or None to stop."""
+        ptr = None if stamps is None else _native.c_vp(stamps.data_ptr())
+        check(_native.lib().deft_comm_set_phase_trace(self._h, ptr), "deft_comm_set_phase_trace")
+
     def _exchange(self, group) -> PeerMaps:
         import torch.distributed as dist
         mine = [bytes(r.handle) for r in (self._g, self._p, self._f)]

@@ -99,6 +99,12 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 
+// Diagnostics: globaltimer stamp of phase k of this block (deft_comm_set_phase_trace)
+__device__ __forceinline__ void phase_stamp(const PeerPtrs& P, int k) {
+  if (P.phase_ts != nullptr && threadIdx.x == 0 && blockIdx.y == 0)
+    P.phase_ts[(int64_t)blockIdx.x * kPhases + k] = global_ns();
+}
+
 // Block-level barrier with the same-index block on every rank.  The spin is
 // bounded by P.spin_timeout_ns: a peer block that never arrives (a launch whose
 // blocks cannot all be resident, a rank that died) traps with a message.
@@ -106,6 +112,7 @@ __device__ __forceinline__ void peer_block_barrier(const PeerPtrs& P, int rank, 
                                                    int set, int block, uint32_t value) {
   __threadfence_system();
   __syncthreads();
+  if (P.no_peer_barrier) return;   // profiling only (common.cuh)
   if ((int)threadIdx.x < world) {
     const int peer = threadIdx.x;
     const int64_t base = ((int64_t)set * kMaxCommBlocks + block) * kMaxWorld;
@@ -1000,8 +1007,11 @@ __global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
   __shared__ __align__(8) uint64_t full[kTmaStages];
   // elements per peer chunk: a stage holds W chunks, 16-byte granular
   constexpr int64_t kChunk = rs_tma_chunk<T, W>();
+  phase_stamp(P, 0);
   const uint32_t epoch = take_epochs(P, rank, kBarrierRS, 1u) + 1u;
+  phase_stamp(P, 1);
   peer_block_barrier(P, rank, W, kBarrierRS, blockIdx.x, epoch);
+  phase_stamp(P, 2);
   // the barrier's acquire is a generic-proxy operation; the peers' gradient
   // bytes are read by the async proxy (cp.async.bulk): order the two
   if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -1055,6 +1065,7 @@ __global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
     // keep the ring full: chunk c + S - 1 goes into the stage freed at the end of c - 1
     if (threadIdx.x == 0 && c + kTmaStages - 1 < c_end) issue(c + kTmaStages - 1);
     mbar_wait(&full[st], parity);
+    if (c == c_begin) phase_stamp(P, 3);
     int64_t e0, len;
     table_chunk(t, kChunk, c, &e0, &len);
     using Raw = typename V::Raw;
@@ -1071,6 +1082,7 @@ __global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
     }
     __syncthreads();  // stage st fully consumed before it is refilled
   }
+  phase_stamp(P, 6);
 }
 
 template <typename T, int S>
@@ -1231,8 +1243,11 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
   extern __shared__ __align__(128) unsigned char usmem[];
   __shared__ __align__(8) uint64_t full[kUpdTmaStages];
 
+  phase_stamp(P, 0);
   const uint32_t epoch = take_epochs(P, rank, kBarrierUpdate, 2u);
+  phase_stamp(P, 1);
   peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 1u);
+  phase_stamp(P, 2);
   // generic acquire -> async-proxy (bulk copy) accesses of global memory
   if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
   const T* g = reinterpret_cast<const T*>(P.grads[rank]) + slot_base;
@@ -1294,6 +1309,7 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
     const uint32_t parity = (uint32_t)(((c - c_begin) / kUpdTmaStages) & 1);
     if (threadIdx.x == 0 && c + kAhead < c_end) issue_load(c + kAhead);
     mbar_wait(&full[st], parity);
+    if (c == c_begin) phase_stamp(P, 3);
     int64_t e0, len;
     chunk_range(c, &e0, &len);
     const T* sg = reinterpret_cast<const T*>(base(st));
@@ -1332,12 +1348,15 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
       tma_store_commit();
     }
   }
+  phase_stamp(P, 4);
   if (threadIdx.x == 0) {
     tma_store_wait_all();  // every bulk store of this CTA performed (incl. peers)
     asm volatile("fence.proxy.async.global;" ::: "memory");
   }
+  phase_stamp(P, 5);
   // exit: every rank's stores into every parameter buffer have landed
   peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 2u);
+  phase_stamp(P, 6);
 }
 
 // DEFT_UPDATE_TMA_PIPE=S:P -> 30 (3:0), 41 (4:1, default) or 62 (6:2)
@@ -1555,9 +1574,12 @@ __global__ void __launch_bounds__(kOneShotThreads) oneshot_update_kernel(
   using Raw = typename V::Raw;
   constexpr int N = V::N;
   constexpr bool kMaster = sizeof(T) == 2;
+  phase_stamp(P, 0);
   const uint32_t epoch = take_epochs(P, rank, kBarrierUpdate, 2u);
+  phase_stamp(P, 1);
   // entry: every rank's slot holds this group's complete gradient
   peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 1u);
+  phase_stamp(P, 2);
   const T* src[W];
 #pragma unroll
   for (int k = 0; k < W; ++k) src[k] = reinterpret_cast<const T*>(P.grads[k]) + slot_base;
@@ -1640,8 +1662,10 @@ __global__ void __launch_bounds__(kOneShotThreads) oneshot_update_kernel(
       reinterpret_cast<Raw*>(dst + e)[0] = V::from_f32(pp);
     }
   }
+  phase_stamp(P, 4);
   // exit: no peer reads this rank's slot any more (it may be recycled)
   peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 2u);
+  phase_stamp(P, 6);
 }
 
 // DEFT_ONESHOT_BLOCKS: CTA cap of the one-shot kernel (default 128)

@@ -352,6 +352,14 @@ extern "C" deft_status_t deft_comm_create(int32_t rank, int32_t world, void* con
   c->P.master = grad_dtype == DEFT_DTYPE_BF16 ? d_master : nullptr;
   c->P.grid_cap = 0;
   c->P.spin_timeout_ns = default_spin_timeout_ns();
+  c->P.phase_ts = nullptr;
+  {
+    const char* e = getenv("DEFT_PROFILE_NO_PEER_BARRIER");
+    c->P.no_peer_barrier = e && atoi(e) == 1;
+    if (c->P.no_peer_barrier)
+      fprintf(stderr, "deft: DEFT_PROFILE_NO_PEER_BARRIER=1 -- peer barriers disabled, "
+                      "results are racy (profiling only)\n");
+  }
   c->rank = rank;
   c->world = world;
   c->dtype = grad_dtype;
@@ -398,6 +406,12 @@ extern "C" deft_status_t deft_comm_configure(deft_comm* c, int32_t grid_cap,
     return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_comm_configure");
   if (grid_cap >= 0) c->P.grid_cap = grid_cap;
   if (spin_timeout_ms >= 0) c->P.spin_timeout_ns = (uint64_t)spin_timeout_ms * 1000000ull;
+  return DEFT_OK;
+}
+
+extern "C" deft_status_t deft_comm_set_phase_trace(deft_comm* c, uint64_t* dev_stamps) {
+  if (!c) return fail(DEFT_ERR_INVALID_ARGUMENT, "deft_comm_set_phase_trace");
+  c->P.phase_ts = dev_stamps;
   return DEFT_OK;
 }
 

@@ -51,7 +51,16 @@ struct PeerPtrs {
   // a barrier spin longer than this traps (0 = unbounded): a peer that never
   // arrives becomes a loud kernel fault instead of a hung GPU
   uint64_t spin_timeout_ns;
+  // PROFILING ONLY (DEFT_PROFILE_NO_PEER_BARRIER=1): peer barriers return at once,
+  // so a kernel profiler can replay one rank's launch without its peers (the
+  // results are then racy -- never set outside an ncu capture)
+  int32_t no_peer_barrier;
+  // DIAGNOSTICS (deft_comm_set_phase_trace): when set, thread 0 of every block of
+  // the TMA reduce-scatter / TMA update / one-shot kernels stores globaltimer
+  // stamps at phase boundaries: phase_ts[block * kPhases + k]
+  uint64_t* phase_ts;
 };
+constexpr int kPhases = 8;  // start | epoch | entry barrier | first data | body | drain | exit
 
 // grid of a peer-barrier kernel after the communicator's cap
 __host__ inline int cap_grid(const PeerPtrs& P, int grid) {

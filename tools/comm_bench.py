@@ -52,6 +52,39 @@ def timeit(fn, reps, warm, stream, device):
     return float(t.item())
 
 
+PHASE_NAMES = ["start", "epoch", "entry_barrier", "first_stage", "body", "drain", "end"]
+
+
+def phases(comm, fn, stream, device):
+    """Two back-to-back launches of fn with phase stamps (ns) -> per phase the
+    median / max over blocks of (stamp - the launch's earliest start), us, plus
+    the gap from the first launch's last block end to the second's first start."""
+    bufs = [torch.zeros(256 * 8, dtype=torch.int64, device=device) for _ in range(2)]
+    torch.cuda.synchronize()
+    dist.barrier()
+    for b in bufs:
+        comm.set_phase_trace(b)
+        fn()
+    comm.set_phase_trace(None)
+    torch.cuda.synchronize()
+    out = {}
+    ends = []
+    for i, b in enumerate(bufs):
+        st = b.view(256, 8).cpu().tolist()
+        rows = [r for r in st if r[0] > 0]
+        t0 = min(r[0] for r in rows)
+        ph = {}
+        for k, name in enumerate(PHASE_NAMES):
+            d = sorted((r[k] - t0) / 1e3 for r in rows if r[k] > 0)
+            if d:
+                ph[name] = [round(d[len(d) // 2], 2), round(d[-1], 2)]
+        ph["blocks"] = len(rows)
+        out[f"launch{i}"] = ph
+        ends.append((t0, max(r[6] for r in rows if r[6] > 0)))
+    out["gap_us"] = round((ends[1][0] - ends[0][1]) / 1e3, 2)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes-mb", default="1,4,16,64,256")
@@ -61,6 +94,10 @@ def main():
     ap.add_argument("--check", action="store_true",
                     help="verify every reduce-scatter result before timing")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--phases", action="store_true",
+                    help="per-phase globaltimer stamps of every block (deft_comm_set_phase_trace): "
+                         "start -> epoch -> entry barrier -> first stage -> body -> drain -> end, "
+                         "and the gap between two back-to-back launches")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -105,6 +142,8 @@ def main():
             }
             for key, fn in kernels.items():
                 res[f"{key}_ms"] = timeit(fn, args.reps, 3, s, dev)
+                if args.phases and key != "rs_ce":
+                    res.setdefault("phases_us", {})[key] = phases(comm, fn, s, dev)
 
             def deft():
                 comm.reduce_scatter(_native.CHANNEL_SM, 0, 0, n, s)
