@@ -108,9 +108,17 @@ __device__ __forceinline__ void phase_stamp(const PeerPtrs& P, int k) {
 // Block-level barrier with the same-index block on every rank.  The spin is
 // bounded by P.spin_timeout_ns: a peer block that never arrives (a launch whose
 // blocks cannot all be resident, a rank that died) traps with a message.
+//
+// Ordering: the flag store is st.release.sys (fence.acq_rel.sys + store) by the
+// signalling thread after bar.sync, so every write of the CTA that precedes the
+// bar.sync is ordered before it (release cumulativity through the CTA-scope
+// barrier -- the cooperative-groups grid-sync pattern); the acquire spin + the
+// closing bar.sync order the peers' writes before every thread's later reads.
+// DEFT_BARRIER_FENCE=all restores a per-thread membar.sys before the bar.sync
+// (round-1 behaviour, kept for A/B).
 __device__ __forceinline__ void peer_block_barrier(const PeerPtrs& P, int rank, int world,
                                                    int set, int block, uint32_t value) {
-  __threadfence_system();
+  if (P.barrier_fence_all) __threadfence_system();
   __syncthreads();
   if (P.no_peer_barrier) return;   // profiling only (common.cuh)
   if ((int)threadIdx.x < world) {
@@ -1244,12 +1252,6 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
   __shared__ __align__(8) uint64_t full[kUpdTmaStages];
 
   phase_stamp(P, 0);
-  const uint32_t epoch = take_epochs(P, rank, kBarrierUpdate, 2u);
-  phase_stamp(P, 1);
-  peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 1u);
-  phase_stamp(P, 2);
-  // generic acquire -> async-proxy (bulk copy) accesses of global memory
-  if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
   const T* g = reinterpret_cast<const T*>(P.grads[rank]) + slot_base;
   float* ref = kMaster ? (kLoop ? slices[blockIdx.y].master : P.master)
                        : reinterpret_cast<float*>(P.params[rank]);
@@ -1257,23 +1259,6 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
 #pragma unroll
   for (int k = 0; k < W; ++k) dst[k] = reinterpret_cast<T*>(P.params[k]);
 
-  // unaligned edges of every segment: block 0, scalar
-  if (blockIdx.x == 0) {
-    for (int sgi = 0; sgi < t.count; ++sgi) {
-      for (int part = 0; part < 2; ++part) {
-        const int64_t a = part ? t.tail_lo[sgi] : t.head_lo[sgi];
-        const int64_t b = part ? t.tail_hi[sgi] : t.head_hi[sgi];
-        for (int64_t e = a + threadIdx.x; e < b; e += blockDim.x) {
-          const float v = fmaf(momentum, mom[e], V::scalar(g + e) * scale);
-          mom[e] = v;
-          const float p = fmaf(-lr, v, ref[e]);
-          if (kMaster) ref[e] = p;
-#pragma unroll
-          for (int k = 0; k < W; ++k) store1(dst[k] + e, p);
-        }
-      }
-    }
-  }
   const int64_t n_chunks = t.first[t.count];
   const int64_t c_begin = n_chunks * blockIdx.x / gridDim.x;
   const int64_t c_end = n_chunks * (blockIdx.x + 1) / gridDim.x;
@@ -1281,7 +1266,6 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
     for (int st = 0; st < kUpdTmaStages; ++st) mbar_init(&full[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
   auto chunk_range = [&](int64_t c, int64_t* e0, int64_t* len) {
     table_chunk(t, kUpdChunk, c, e0, len);
   };
@@ -1302,8 +1286,36 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
     tma_load_1d(base(st) + kG, mom + e0, bf, &full[st]);
     tma_load_1d(base(st) + kG + kF, ref + e0, bf, &full[st]);
   };
+  // The first stages read only this rank's own gradient shard, momentum and
+  // parameter shard (stream-ordered, never written by a peer): they are issued
+  // BEFORE the entry barrier so its NVLink round trip overlaps their HBM latency.
+  // Only the stores into the peers' parameter buffers must wait for it.
   if (threadIdx.x == 0)
     for (int64_t c = c_begin; c < min(c_end, c_begin + kAhead); ++c) issue_load(c);
+  const uint32_t epoch = take_epochs(P, rank, kBarrierUpdate, 2u);  // + bar.sync: mbarriers init'd
+  phase_stamp(P, 1);
+  peer_block_barrier(P, rank, W, kBarrierUpdate, blockIdx.x, epoch + 1u);
+  phase_stamp(P, 2);
+  // generic acquire -> async-proxy (bulk copy) accesses of global memory
+  if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+
+  // unaligned edges of every segment: block 0, scalar
+  if (blockIdx.x == 0) {
+    for (int sgi = 0; sgi < t.count; ++sgi) {
+      for (int part = 0; part < 2; ++part) {
+        const int64_t a = part ? t.tail_lo[sgi] : t.head_lo[sgi];
+        const int64_t b = part ? t.tail_hi[sgi] : t.head_hi[sgi];
+        for (int64_t e = a + threadIdx.x; e < b; e += blockDim.x) {
+          const float v = fmaf(momentum, mom[e], V::scalar(g + e) * scale);
+          mom[e] = v;
+          const float p = fmaf(-lr, v, ref[e]);
+          if (kMaster) ref[e] = p;
+#pragma unroll
+          for (int k = 0; k < W; ++k) store1(dst[k] + e, p);
+        }
+      }
+    }
+  }
   for (int64_t c = c_begin; c < c_end; ++c) {
     const int st = (int)((c - c_begin) % kUpdTmaStages);
     const uint32_t parity = (uint32_t)(((c - c_begin) / kUpdTmaStages) & 1);

@@ -354,6 +354,10 @@ extern "C" deft_status_t deft_comm_create(int32_t rank, int32_t world, void* con
   c->P.spin_timeout_ns = default_spin_timeout_ns();
   c->P.phase_ts = nullptr;
   {
+    const char* e = getenv("DEFT_BARRIER_FENCE");
+    c->P.barrier_fence_all = e && strcmp(e, "all") == 0;
+  }
+  {
     const char* e = getenv("DEFT_PROFILE_NO_PEER_BARRIER");
     c->P.no_peer_barrier = e && atoi(e) == 1;
     if (c->P.no_peer_barrier)

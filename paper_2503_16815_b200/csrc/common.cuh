@@ -55,6 +55,8 @@ struct PeerPtrs {
   // so a kernel profiler can replay one rank's launch without its peers (the
   // results are then racy -- never set outside an ncu capture)
   int32_t no_peer_barrier;
+  // DEFT_BARRIER_FENCE=all: every thread executes membar.sys before a peer barrier
+  int32_t barrier_fence_all;
   // DIAGNOSTICS (deft_comm_set_phase_trace): when set, thread 0 of every block of
   // the TMA reduce-scatter / TMA update / one-shot kernels stores globaltimer
   // stamps at phase boundaries: phase_ts[block * kPhases + k]

@@ -5,7 +5,7 @@
 # first and only profiles it if that exited 0.
 #
 #   bench TAG N [bench.py args]        one bench line (torchrun for N > 1) -> TAG.json
-#   comm N [SIZES_MB]                  tools/comm_bench.py --nvml --check -> comm_nN.jsonl
+#   comm N [SIZES_MB]                  tools/comm_bench.py --check -> comm_nN.jsonl
 #   update_w1                          tools/update_bench.py (sgd_local variants, GPU 0)
 #   launches TAG [profile_step args]   ncu launch list of one step (1 GPU) -> TAG_launches.csv
 #   full TAG KERNEL_REGEX [args]       ncu --set full of one launch of KERNEL -> TAG.ncu-rep + raw csv
@@ -27,7 +27,7 @@ case "$cmd" in
   comm)
     n=$1 sizes=${2:-0.25,1,4,16,64,256}
     timeout 900 $T --nproc-per-node $n --master-port $(port) tools/comm_bench.py --sizes-mb $sizes \
-      --nvml --check > gpurun_out/comm_n$n.jsonl 2> gpurun_out/comm_n$n.err
+      --check > gpurun_out/comm_n$n.jsonl 2> gpurun_out/comm_n$n.err
     echo "comm n=$n rc=$?";;
   update_w1)
     CUDA_VISIBLE_DEVICES=0 timeout 900 python tools/update_bench.py "$@" > gpurun_out/update_w1.jsonl 2>&1
