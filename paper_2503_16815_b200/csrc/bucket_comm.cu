@@ -997,9 +997,12 @@ __device__ __forceinline__ void table_chunk(const ChunkTable& t, int64_t chunk, 
   *len = rem < chunk ? rem : chunk;
 }
 
+// Elements per peer chunk: a stage holds the W-1 PEER chunks only (the own chunk
+// is read from global memory by the consumer threads, prefetched into registers
+// while the stage is in flight), so the whole stage carries NVLink bytes.
 template <typename T, int W>
-__host__ __device__ constexpr int64_t rs_tma_chunk() {  // elements per peer chunk
-  return (kTmaStageBytes / W / (int)sizeof(T)) / 8 * 8;
+__host__ __device__ constexpr int64_t rs_tma_chunk() {
+  return (kTmaStageBytes / (W - 1) / (int)sizeof(T)) / 8 * 8;
 }
 
 // One launch reduces every segment of the table (all buckets released together
@@ -1013,7 +1016,7 @@ __global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
   using V = Vec<T>;
   extern __shared__ __align__(128) unsigned char tma_smem[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
-  // elements per peer chunk: a stage holds W chunks, 16-byte granular
+  // elements per peer chunk: a stage holds the W-1 peer chunks, 16-byte granular
   constexpr int64_t kChunk = rs_tma_chunk<T, W>();
   phase_stamp(P, 0);
   const uint32_t epoch = take_epochs(P, rank, kBarrierRS, 1u) + 1u;
@@ -1050,10 +1053,12 @@ __global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // stage slot of peer k (the own rank has none)
   auto stage_ptr = [&](int st, int k) -> T* {
-    return reinterpret_cast<T*>(tma_smem + (size_t)st * kTmaStageBytes) + (int64_t)k * kChunk;
+    const int slot = k < rank ? k : k - 1;
+    return reinterpret_cast<T*>(tma_smem + (size_t)st * kTmaStageBytes) + (int64_t)slot * kChunk;
   };
-  auto issue = [&](int64_t c) {  // one elected thread: W bulk copies of chunk c
+  auto issue = [&](int64_t c) {  // one elected thread: W-1 bulk copies of chunk c
     const int st = (int)((c - c_begin) % kTmaStages);
     int64_t e0, len;
     table_chunk(t, kChunk, c, &e0, &len);
@@ -1061,28 +1066,46 @@ __global__ void __launch_bounds__(kTmaThreads) reduce_scatter_tma_kernel(
     // the stage was last read through the generic proxy; order that before the
     // async-proxy (TMA) writes that refill it
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&full[st], bytes * W);
+    mbar_expect_tx(&full[st], bytes * (W - 1));
 #pragma unroll
-    for (int k = 0; k < W; ++k) tma_load_1d(stage_ptr(st, k), src[k] + e0, bytes, &full[st]);
+    for (int k = 0; k < W; ++k)
+      if (k != rank) tma_load_1d(stage_ptr(st, k), src[k] + e0, bytes, &full[st]);
   };
   if (threadIdx.x == 0)
     for (int64_t c = c_begin; c < min(c_end, c_begin + kTmaStages - 1); ++c) issue(c);
+  using Raw = typename V::Raw;
+  // vectors of one chunk per thread (the own values are prefetched in registers)
+  constexpr int kPer = (int)((kChunk / V::N + kTmaThreads - 1) / kTmaThreads);
   for (int64_t c = c_begin; c < c_end; ++c) {
     const int st = (int)((c - c_begin) % kTmaStages);
     const uint32_t parity = (uint32_t)(((c - c_begin) / kTmaStages) & 1);
     // keep the ring full: chunk c + S - 1 goes into the stage freed at the end of c - 1
     if (threadIdx.x == 0 && c + kTmaStages - 1 < c_end) issue(c + kTmaStages - 1);
-    mbar_wait(&full[st], parity);
-    if (c == c_begin) phase_stamp(P, 3);
     int64_t e0, len;
     table_chunk(t, kChunk, c, &e0, &len);
-    using Raw = typename V::Raw;
-    for (int64_t v = threadIdx.x; v < len / V::N; v += blockDim.x) {
+    const int64_t nv = len / V::N;
+    // own chunk: plain loads (this kernel writes these same elements below, each
+    // thread only its own) issued before the wait so they overlap the stage's flight
+    Raw own[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int64_t v = threadIdx.x + (int64_t)j * kTmaThreads;
+      if (v < nv) own[j] = reinterpret_cast<const Raw*>(dst + e0)[v];
+    }
+    mbar_wait(&full[st], parity);
+    if (c == c_begin) phase_stamp(P, 3);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int64_t v = threadIdx.x + (int64_t)j * kTmaThreads;
+      if (v >= nv) break;
+      // rank order, exactly as before: acc = x_0 + x_1 + ... + x_{W-1}
       float acc[V::N], tmp[V::N];
-      V::to_f32(reinterpret_cast<const Raw*>(stage_ptr(st, 0))[v], acc);
+      if (rank == 0) V::to_f32(own[j], acc);
+      else V::to_f32(reinterpret_cast<const Raw*>(stage_ptr(st, 0))[v], acc);
 #pragma unroll
       for (int k = 1; k < W; ++k) {
-        V::to_f32(reinterpret_cast<const Raw*>(stage_ptr(st, k))[v], tmp);
+        if (k == rank) V::to_f32(own[j], tmp);
+        else V::to_f32(reinterpret_cast<const Raw*>(stage_ptr(st, k))[v], tmp);
 #pragma unroll
         for (int q = 0; q < V::N; ++q) acc[q] += tmp[q];
       }
@@ -1156,7 +1179,7 @@ static int rs_tma_blocks() {
 
 static int64_t rs_chunk_for(int world, int dtype) {
   const int esz = dtype == 0 ? 4 : 2;
-  return (kTmaStageBytes / world / esz) / 8 * 8;   // == rs_tma_chunk<T, W>()
+  return (kTmaStageBytes / (world - 1) / esz) / 8 * 8;   // == rs_tma_chunk<T, W>()
 }
 
 bool launch_reduce_scatter_tma_multi(const PeerPtrs& P, int rank, int world, int dtype,
@@ -1615,6 +1638,7 @@ __global__ void __launch_bounds__(kOneShotThreads) oneshot_update_kernel(
   for (int64_t u0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u0 < total;
        u0 += stride * kOneShotUnroll) {
     Raw raw[kOneShotUnroll][W];
+    float4 m4s[kOneShotUnroll][N / 4], p4s[kOneShotUnroll][N / 4];
     int64_t el[kOneShotUnroll];
     float sc[kOneShotUnroll];
     bool vec[kOneShotUnroll];
@@ -1638,6 +1662,12 @@ __global__ void __launch_bounds__(kOneShotThreads) oneshot_update_kernel(
         vec[q] = true;
 #pragma unroll
         for (int r = 0; r < W; ++r) raw[q][r] = ld_nc(reinterpret_cast<const Raw*>(src[r] + e));
+        // the local momentum / fp32 parameters ride along with the peer loads
+#pragma unroll
+        for (int c = 0; c < N / 4; ++c) {
+          m4s[q][c] = load4(mom + e + 4 * c);
+          p4s[q][c] = load4(ref + e + 4 * c);
+        }
       } else {
         for (int64_t x = e; x < end; ++x) one(x, sc[q]);                     // tail
       }
@@ -1658,8 +1688,8 @@ __global__ void __launch_bounds__(kOneShotThreads) oneshot_update_kernel(
       float vv[N], pp[N];
 #pragma unroll
       for (int c = 0; c < N; c += 4) {
-        const float4 m4 = load4(mom + e + c);
-        const float4 p4 = load4(ref + e + c);
+        const float4 m4 = m4s[q][c / 4];
+        const float4 p4 = p4s[q][c / 4];
         vv[c + 0] = fmaf(momentum, m4.x, acc[c + 0] * sc[q]);
         vv[c + 1] = fmaf(momentum, m4.y, acc[c + 1] * sc[q]);
         vv[c + 2] = fmaf(momentum, m4.z, acc[c + 2] * sc[q]);

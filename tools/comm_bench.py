@@ -35,16 +35,30 @@ from paper_2503_16815_b200 import _native  # noqa: E402
 from paper_2503_16815_b200.comm import BucketComm  # noqa: E402
 
 
-def timeit(fn, reps, warm, stream, device):
-    """ms per call, CUDA events on `stream`, after a barrier, max over ranks."""
+def timeit(fn, reps, warm, stream, device, graph=False):
+    """ms per call, CUDA events on `stream`, after a barrier, max over ranks.
+    graph: the reps calls are captured into one CUDA graph and replayed (no host
+    launch cost between calls -- the way the training step issues them)."""
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
+    run = None
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(reps):
+                fn()
+        g.replay()                      # warm replay
+        torch.cuda.synchronize()
+        run = g.replay
     dist.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
-    for _ in range(reps):
-        fn()
+    if run is not None:
+        run()
+    else:
+        for _ in range(reps):
+            fn()
     b.record(stream)
     torch.cuda.synchronize()
     t = torch.tensor([a.elapsed_time(b) / reps], device=device)
@@ -94,6 +108,9 @@ def main():
     ap.add_argument("--check", action="store_true",
                     help="verify every reduce-scatter result before timing")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="time every variant as a CUDA graph of --reps calls (device time "
+                         "without host launch cost); keys *_ms then are graph times")
     ap.add_argument("--phases", action="store_true",
                     help="per-phase globaltimer stamps of every block (deft_comm_set_phase_trace): "
                          "start -> epoch -> entry barrier -> first stage -> body -> drain -> end, "
@@ -115,7 +132,7 @@ def main():
     for mb in sizes:
         n = int(mb * 2**20) // 4
         nbytes = n * 4
-        res = {"bucket_mb": mb, "world": W}
+        res = {"bucket_mb": mb, "world": W, "timing": "cuda graph" if args.graph else "eager"}
         if args.check:
             for ch in (_native.CHANNEL_SM, _native.CHANNEL_CE):
                 idx = torch.arange(n, device=dev, dtype=torch.float32)
@@ -141,25 +158,25 @@ def main():
                 "oneshot": lambda: comm.sync_update_multi(0, [(0, n)], 1e-3, 1e-9, 0.9, mom, s),
             }
             for key, fn in kernels.items():
-                res[f"{key}_ms"] = timeit(fn, args.reps, 3, s, dev)
+                res[f"{key}_ms"] = timeit(fn, args.reps, 3, s, dev, args.graph)
                 if args.phases and key != "rs_ce":
                     res.setdefault("phases_us", {})[key] = phases(comm, fn, s, dev)
 
             def deft():
                 comm.reduce_scatter(_native.CHANNEL_SM, 0, 0, n, s)
                 comm.update_multi(0, [(0, n)], 1e-3, 1e-9, 0.9, mom, s)
-            res["deft_ms"] = timeit(deft, args.reps, 3, s, dev)
+            res["deft_ms"] = timeit(deft, args.reps, 3, s, dev, args.graph)
             if not args.no_nccl:
                 x = torch.randn(n, device=dev)
                 p = torch.randn(n, device=dev)
                 v = torch.zeros(n, device=dev)
-                res["nccl_ar_ms"] = timeit(lambda: dist.all_reduce(x), args.reps, 3, s, dev)
+                res["nccl_ar_ms"] = timeit(lambda: dist.all_reduce(x), args.reps, 3, s, dev, args.graph)
 
                 def nccl_sgd():
                     dist.all_reduce(x)
                     v.mul_(0.9).add_(x, alpha=1e-3)
                     p.add_(v, alpha=-1e-9)
-                res["nccl_ar_sgd_ms"] = timeit(nccl_sgd, args.reps, 3, s, dev)
+                res["nccl_ar_sgd_ms"] = timeit(nccl_sgd, args.reps, 3, s, dev, args.graph)
         frac = (W - 1) / W
         res["rs_sm_busbw_gbs"] = round(frac * nbytes / res["rs_sm_ms"] / 1e6, 1)
         res["rs_ce_busbw_gbs"] = round(frac * nbytes / res["rs_ce_ms"] / 1e6, 1)

@@ -8,7 +8,7 @@
 out=$1 k=$2; shift 2
 export DEFT_PROFILE_NO_PEER_BARRIER=1
 if [ "${LOCAL_RANK:-0}" = 0 ]; then
-  ncu --set full --clock-control none --import-source on -k "regex:$k" -s ${NCU_SKIP:-4} -c 1 \
+  ncu --set full --clock-control none --import-source on -k "regex:$k" -s ${NCU_SKIP:-2} -c 1 \
     -o "$out" "$@"
   rc=$?
   ncu -i "$out.ncu-rep" --page raw --csv > "$out.raw.csv" 2>&1
