@@ -536,12 +536,18 @@ def ddp_baseline(args, world, rank, device, dist):
     loss_fn = loss_fn_for(args.model)
     batch = make_batch(args.model, args.batch, device, seed=1234 + rank)
     bucket_mb = args.bucket_mb or 25
+    # graphed arm: DDP is built, warmed up and captured on ONE side stream (its
+    # reducer keeps the AccumulateGrad nodes of the first iterations alive, and a
+    # node created on another stream breaks the capture)
+    s = torch.cuda.Stream(device) if args.ddp_graphs else torch.cuda.current_stream(device)
+    s.wait_stream(torch.cuda.current_stream(device))
     net = model
-    if world > 1:
-        net = torch.nn.parallel.DistributedDataParallel(
-            model, device_ids=[device.index], bucket_cap_mb=bucket_mb,
-            gradient_as_bucket_view=True, static_graph=args.ddp_graphs)
-    opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9, fused=True)
+    with torch.cuda.stream(s):
+        if world > 1:
+            net = torch.nn.parallel.DistributedDataParallel(
+                model, device_ids=[device.index], bucket_cap_mb=bucket_mb,
+                gradient_as_bucket_view=True, static_graph=args.ddp_graphs)
+        opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9, fused=True)
     amp = next(model.parameters()).dtype == torch.float32
 
     def step():
@@ -551,21 +557,20 @@ def ddp_baseline(args, world, rank, device, dist):
             loss = loss_fn(net, batch)
         loss.backward()
         opt.step()
+        return loss
 
     clk = ClockSampler(device.index).__enter__()
     mode = "eager"
     run = step
     if args.ddp_graphs:
-        s = torch.cuda.Stream(device)
-        s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
-            for _ in range(max(3, args.warmup)):
-                step()
-        torch.cuda.current_stream().wait_stream(s)
+            for _ in range(max(11, args.warmup)):   # DDP settles its buckets first
+                loss = step()
+        del loss
         torch.cuda.synchronize()
         try:
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
                 step()
             run, mode = g.replay, "cuda_graph"
         except Exception as e:   # reported, the eager step is timed instead
@@ -636,6 +641,9 @@ def main():
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
+        if args.impl == "ddp" and args.ddp_graphs:
+            # no watchdog event queries against a capturing stream
+            os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "0")
         init_quiet(dist, device)
     torch.backends.cudnn.benchmark = True
     if args.impl == "ddp":
