@@ -27,8 +27,7 @@ def main():
     model = bench.build_model(args.model, dev)
     loss_fn = bench.loss_fn_for(args.model)
     batch = bench.make_batch(args.model, 64, dev)
-    walk = D.WalkParams.from_dict(
-        json.loads((ROOT / "tests" / "golden" / "inputs.json").read_text())["walk"])
+    walk = D.WalkParams.from_dict(bench.DEFAULT_WALK)
     cfg = D.DeftConfig(lr=0.1, momentum=0.9, walk=walk, cuda_graphs=not args.eager,
                        partition=D.PartitionConfig(partition_size=6_500_000, mu=1.0))
     ddp = D.DeftDataParallel(model, cfg)
