@@ -607,6 +607,15 @@ def ddp_baseline(args, world, rank, device, dist):
                                    f"batch {args.batch}/GPU", "bucket_cap_mb": bucket_mb,
                        "mode": mode},
             "clocks": clk.summary()}))
+    if args.ddp_graphs:
+        # a communicator captured into a CUDA graph hangs in its teardown (measured:
+        # the line is printed, then destroy_process_group never returns)
+        sys.stdout.flush()
+        sys.stderr.flush()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        os._exit(0)
     if world > 1:
         dist.destroy_process_group()
 

@@ -289,3 +289,35 @@ def test_loopback_deferral_policies(world, defer, dtype):
     the trajectory: the link-queue model (comm 900 us per bucket against 150 us
     of backward each) defers most of them, False none."""
     _check(world, 14, dtype=dtype, placement="start", cuda_graphs=True, defer=defer)
+
+
+def test_loopback_phase_stamps():
+    """deft_comm_set_phase_trace (diagnostics): every block of the collective
+    reduce-scatter and update launches stamps its phases in order (start <=
+    epoch <= entry barrier <= first stage <= end), and stamping leaves the
+    results unchanged."""
+    from paper_2503_16815_b200 import _native
+    world = 2
+    lbw = S.D.LoopbackWorld(world)
+    n = 1 << 20
+    comms = lbw.make_comms(1, n, torch.float32)
+    dev = lbw.device
+    for r, c in enumerate(comms):
+        c.grads[0].copy_(torch.full((n,), float(r + 1), device=dev))
+    stream = torch.cuda.Stream(dev)
+    stamps = torch.zeros(256 * 8, dtype=torch.int64, device=dev)
+    comms[0].set_phase_trace(stamps)
+    lbw.collective_reduce_scatter(comms, _native.CHANNEL_SM, 0, [(0, n)], stream)
+    torch.cuda.synchronize()
+    comms[0].set_phase_trace(None)
+    st = stamps.view(256, 8).cpu()
+    used = st[st[:, 0] > 0]
+    assert len(used) > 0
+    for row in used.tolist():
+        seq = [row[k] for k in (0, 1, 2, 3, 6)]
+        assert seq == sorted(seq), row
+    # rank 0 owns the first shard: 1 + 2 everywhere in it
+    lo, hi = S.shard_range(0, n, 0, world, 4)
+    assert torch.all(comms[0].grads[0][lo:hi] == 3.0)
+    for c in comms:
+        c.close()
