@@ -59,7 +59,11 @@ def test_hw_experiment_reports(tmp_path):
     want = json.loads((REP / "summary.json").read_text())
     assert set(got) == set(want)
     assert got["config_hash"] == X.config_hash(cfg, 0)
-    assert {set(r) == set(want["runs"][0]) for r in got["runs"]} == {True}
+    # every run: exactly the reference's keys, plus this runner's "hardware" block
+    # (world, buckets, links, compute-only step, placement) that only a run on GPUs has
+    assert {set(r) - {"hardware"} == set(want["runs"][0]) for r in got["runs"]} == {True}
+    assert all({"world", "buckets", "compute_only_ms_per_step"} <= set(r["hardware"])
+               for r in got["runs"])
     for r in got["runs"]:
         assert r["report"]["total_time_us"] > 0
         if r["scheme"].startswith("deft"):
