@@ -1237,7 +1237,8 @@ constexpr int kUpdTmaThreads = 256;
 // drain at NVLink latency)
 constexpr int kUpdTmaStagesDefault = 4;
 constexpr int kUpdTmaPendingDefault = 1;
-constexpr int kUpdChunk = 2048;  // elements per chunk (multiple of 8)
+constexpr int kUpdChunk = 2048;  // elements per chunk (multiple of 8); DEFT_UPDATE_TMA_CHUNK=4096
+                                 // selects the double-size chunk (4:1 ring only)
 
 __device__ __forceinline__ void tma_store_1d(void* dst_gmem, const void* src_smem,
                                              uint32_t bytes) {
@@ -1257,7 +1258,8 @@ __device__ __forceinline__ void tma_store_wait_all() {
 }
 
 
-template <typename T, int W, int kUpdTmaStages, int kPending, bool kLoop = false>
+template <typename T, int W, int kUpdTmaStages, int kPending, bool kLoop = false,
+          int kChunkE = kUpdChunk>
 __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
     PeerPtrs P, int rank_arg, int64_t slot_base, const __grid_constant__ ChunkTable t_arg,
     float lr, float momentum, float scale, float* __restrict__ mom_arg,
@@ -1268,8 +1270,8 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
   using V = Vec<T>;
   constexpr bool kMaster = sizeof(T) == 2;
   // stage layout: g (T) | v (f32) | p (f32) | p_out (T, bf16 only)
-  constexpr int64_t kG = (int64_t)kUpdChunk * sizeof(T);
-  constexpr int64_t kF = (int64_t)kUpdChunk * 4;
+  constexpr int64_t kG = (int64_t)kChunkE * sizeof(T);
+  constexpr int64_t kF = (int64_t)kChunkE * 4;
   constexpr int64_t kStage = kG + 2 * kF + (kMaster ? kG : 0);
   extern __shared__ __align__(128) unsigned char usmem[];
   __shared__ __align__(8) uint64_t full[kUpdTmaStages];
@@ -1290,7 +1292,7 @@ __global__ void __launch_bounds__(kUpdTmaThreads) update_allgather_tma_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   auto chunk_range = [&](int64_t c, int64_t* e0, int64_t* len) {
-    table_chunk(t, kUpdChunk, c, e0, len);
+    table_chunk(t, kChunkE, c, e0, len);
   };
   auto base = [&](int st) { return usmem + (size_t)st * kStage; };
   static_assert(kPending >= 0 && kPending <= kUpdTmaStages - 2, "ring too small");
@@ -1405,6 +1407,21 @@ static int upd_tma_pipe() {
   return v;
 }
 
+// DEFT_UPDATE_TMA_CHUNK: elements per ring chunk of the update kernel, 2048
+// (default) or 4096 (with the 4:1 ring: 4 x 48 KB of shared memory for fp32)
+static int upd_chunk() {
+  static int v = [] {
+    const char* e = getenv("DEFT_UPDATE_TMA_CHUNK");
+    return e && atoi(e) == 4096 ? 4096 : kUpdChunk;
+  }();
+  return v;
+}
+
+static size_t upd_stage_bytes(int chunk, int dtype) {
+  const size_t esz = dtype == 0 ? 4 : 2;
+  return (size_t)chunk * esz + 2 * (size_t)chunk * 4 + (dtype == 0 ? 0 : (size_t)chunk * esz);
+}
+
 bool launch_update_allgather_tma(const PeerPtrs& P, int rank, int world, int dtype,
                                  int64_t slot_base, int32_t count, const int64_t* offsets,
                                  const int64_t* numels, float lr, float momentum,
@@ -1417,28 +1434,29 @@ bool launch_update_allgather_tma(const PeerPtrs& P, int rank, int world, int dty
   if (!enabled || world < 2) return false;
   const int align = dtype == 0 ? 4 : 8;
   for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
+    const int pipe = upd_tma_pipe();
+    const int chunk = pipe == 41 ? upd_chunk() : kUpdChunk;
     ChunkTable t{};
-    build_chunk_table(t, s0, count, offsets, numels, rank, world, align, kUpdChunk);
+    build_chunk_table(t, s0, count, offsets, numels, rank, world, align, chunk);
     int64_t total_elems = 0;
     for (int k = 0; k < t.count; ++k) total_elems += numels[s0 + k];
     int grid = comm_grid_for((total_elems + world - 1) / world);
     if (max_blocks > 0 && grid > max_blocks) grid = max_blocks;
     grid = cap_grid(P, grid);
-    const size_t esz = dtype == 0 ? 4 : 2;
-    const int pipe = upd_tma_pipe();
-    const size_t smem = (size_t)(pipe / 10) *
-                        (kUpdChunk * esz + 2 * kUpdChunk * 4 + (dtype == 0 ? 0 : kUpdChunk * esz));
-#define DEFT_UPT_LAUNCH(TT, WW, SS, PP)                                                        \
+    const size_t smem = (size_t)(pipe / 10) * upd_stage_bytes(chunk, dtype);
+#define DEFT_UPT_LAUNCH(TT, WW, SS, PP, CC)                                                    \
   {                                                                                            \
-    cudaFuncSetAttribute(update_allgather_tma_kernel<TT, WW, SS, PP>,                          \
+    cudaFuncSetAttribute(update_allgather_tma_kernel<TT, WW, SS, PP, false, CC>,               \
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
-    update_allgather_tma_kernel<TT, WW, SS, PP><<<grid, kUpdTmaThreads, smem, stream>>>(       \
-        P, rank, slot_base, t, lr, momentum, grad_scale, mom, nullptr);                        \
+    update_allgather_tma_kernel<TT, WW, SS, PP, false, CC>                                     \
+        <<<grid, kUpdTmaThreads, smem, stream>>>(P, rank, slot_base, t, lr, momentum,          \
+                                                 grad_scale, mom, nullptr);                    \
   }
 #define DEFT_UPT_PIPE(TT, WW)                                                                  \
-  if (pipe == 30) DEFT_UPT_LAUNCH(TT, WW, 3, 0)                                                \
-  else if (pipe == 62) DEFT_UPT_LAUNCH(TT, WW, 6, 2)                                           \
-  else DEFT_UPT_LAUNCH(TT, WW, 4, 1)
+  if (pipe == 30) DEFT_UPT_LAUNCH(TT, WW, 3, 0, kUpdChunk)                                     \
+  else if (pipe == 62) DEFT_UPT_LAUNCH(TT, WW, 6, 2, kUpdChunk)                                \
+  else if (chunk == 4096) DEFT_UPT_LAUNCH(TT, WW, 4, 1, 4096)                                  \
+  else DEFT_UPT_LAUNCH(TT, WW, 4, 1, kUpdChunk)
 #define DEFT_UPT_CASE(WW)                                                                      \
   case WW:                                                                                     \
     if (dtype == 0) { DEFT_UPT_PIPE(float, WW) } else { DEFT_UPT_PIPE(__nv_bfloat16, WW) }     \
@@ -1535,8 +1553,9 @@ cudaError_t launch_update_tma_loopback(const PeerPtrs& P, int world, int dtype,
   for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
     std::vector<RankSlice> h(world);
     int64_t total_elems = 0;
+    const int chunk = upd_chunk();   // the production ring (4:1) and chunk
     for (int r = 0; r < world; ++r) {
-      build_chunk_table(h[r].t, s0, count, offsets, numels, r, world, align, kUpdChunk);
+      build_chunk_table(h[r].t, s0, count, offsets, numels, r, world, align, chunk);
       h[r].mom = moms[r];
       h[r].master = masters[r];
     }
@@ -1547,23 +1566,26 @@ cudaError_t launch_update_tma_loopback(const PeerPtrs& P, int world, int dtype,
     RankSlice* d = nullptr;
     cudaError_t e = upload_slices(h, &d);
     if (e != cudaSuccess) return e;
-    const size_t esz = dtype == 0 ? 4 : 2;
-    const size_t smem = (size_t)kUpdTmaStagesDefault *
-                        (kUpdChunk * esz + 2 * kUpdChunk * 4 + (dtype == 0 ? 0 : kUpdChunk * esz));
-#define DEFT_UPL_LAUNCH(TT, WW)                                                               \
+    const size_t smem = (size_t)kUpdTmaStagesDefault * upd_stage_bytes(chunk, dtype);
+#define DEFT_UPL_LAUNCH(TT, WW, CC)                                                           \
   {                                                                                           \
     cudaFuncSetAttribute(update_allgather_tma_kernel<TT, WW, kUpdTmaStagesDefault,            \
-                                                     kUpdTmaPendingDefault, true>,            \
+                                                     kUpdTmaPendingDefault, true, CC>,        \
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
-    update_allgather_tma_kernel<TT, WW, kUpdTmaStagesDefault, kUpdTmaPendingDefault, true>    \
+    update_allgather_tma_kernel<TT, WW, kUpdTmaStagesDefault, kUpdTmaPendingDefault, true, CC> \
         <<<dim3(grid, world), kUpdTmaThreads, smem, stream>>>(P, 0, slot_base, h[0].t, lr,    \
                                                               momentum, grad_scale, nullptr,  \
                                                               d);                             \
   }
 #define DEFT_UPL_CASE(WW)                                           \
   case WW:                                                          \
-    if (dtype == 0) DEFT_UPL_LAUNCH(float, WW)                      \
-    else DEFT_UPL_LAUNCH(__nv_bfloat16, WW)                         \
+    if (chunk == 4096) {                                            \
+      if (dtype == 0) DEFT_UPL_LAUNCH(float, WW, 4096)              \
+      else DEFT_UPL_LAUNCH(__nv_bfloat16, WW, 4096)                 \
+    } else {                                                        \
+      if (dtype == 0) DEFT_UPL_LAUNCH(float, WW, kUpdChunk)         \
+      else DEFT_UPL_LAUNCH(__nv_bfloat16, WW, kUpdChunk)            \
+    }                                                               \
     break;
     switch (world) {
       DEFT_UPL_CASE(2) DEFT_UPL_CASE(3) DEFT_UPL_CASE(4) DEFT_UPL_CASE(5)
