@@ -1237,8 +1237,7 @@ constexpr int kUpdTmaThreads = 256;
 // drain at NVLink latency)
 constexpr int kUpdTmaStagesDefault = 4;
 constexpr int kUpdTmaPendingDefault = 1;
-constexpr int kUpdChunk = 2048;  // elements per chunk (multiple of 8); DEFT_UPDATE_TMA_CHUNK=4096
-                                 // selects the double-size chunk (4:1 ring only)
+constexpr int kUpdChunk = 2048;  // elements per chunk (multiple of 8); 4096 at W = 2 (upd_chunk)
 
 __device__ __forceinline__ void tma_store_1d(void* dst_gmem, const void* src_smem,
                                              uint32_t bytes) {
@@ -1407,14 +1406,19 @@ static int upd_tma_pipe() {
   return v;
 }
 
-// DEFT_UPDATE_TMA_CHUNK: elements per ring chunk of the update kernel, 2048
-// (default) or 4096 (with the 4:1 ring: 4 x 48 KB of shared memory for fp32)
-static int upd_chunk() {
-  static int v = [] {
+// Elements per ring chunk of the update kernel (4:1 ring): 4096 at W = 2 (4 x 48
+// KB of shared memory for fp32), else 2048.  Measured at the step's 32-CTA update
+// budget: W = 2, 64 MB 358 -> 431 GB/s, ResNet-101's two start-group launches
+// 272 -> 425 GB/s with the step time unchanged; W = 4 ResNet-101 516 -> 531 GB/s
+// but VGG-19 bs8 in-step 7267 -> 7191 samples/s (profiles/r02h_*, r02i_*).
+// DEFT_UPDATE_TMA_CHUNK=2048|4096 overrides.
+static int upd_chunk(int world) {
+  static int env = [] {
     const char* e = getenv("DEFT_UPDATE_TMA_CHUNK");
-    return e && atoi(e) == 4096 ? 4096 : kUpdChunk;
+    return e ? (atoi(e) == 4096 ? 4096 : kUpdChunk) : 0;
   }();
-  return v;
+  if (env) return env;
+  return world == 2 ? 4096 : kUpdChunk;
 }
 
 static size_t upd_stage_bytes(int chunk, int dtype) {
@@ -1435,7 +1439,7 @@ bool launch_update_allgather_tma(const PeerPtrs& P, int rank, int world, int dty
   const int align = dtype == 0 ? 4 : 8;
   for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
     const int pipe = upd_tma_pipe();
-    const int chunk = pipe == 41 ? upd_chunk() : kUpdChunk;
+    const int chunk = pipe == 41 ? upd_chunk(world) : kUpdChunk;
     ChunkTable t{};
     build_chunk_table(t, s0, count, offsets, numels, rank, world, align, chunk);
     int64_t total_elems = 0;
@@ -1553,7 +1557,7 @@ cudaError_t launch_update_tma_loopback(const PeerPtrs& P, int world, int dtype,
   for (int32_t s0 = 0; s0 < count; s0 += kMaxSeg) {
     std::vector<RankSlice> h(world);
     int64_t total_elems = 0;
-    const int chunk = upd_chunk();   // the production ring (4:1) and chunk
+    const int chunk = upd_chunk(world);   // the production ring (4:1) and chunk
     for (int r = 0; r < world; ++r) {
       build_chunk_table(h[r].t, s0, count, offsets, numels, r, world, align, chunk);
       h[r].mom = moms[r];
