@@ -323,117 +323,7 @@ struct deft_comm {
   char* staging = nullptr;  // CE channel: (W-1) peer shards
   size_t staging_bytes = 0;
   int update_blocks = 0;    // CTA budget of the update kernels (0 = comm default)
-  // CE channel: one copy stream per peer slot so the W-1 peer pulls of a bucket run
-  // on different copy engines at once, and the fork / per-bucket join events
-  cudaStream_t ce_streams[kMaxWorld - 1] = {};
-  cudaEvent_t ce_fork = nullptr;
-  std::vector<cudaEvent_t> ce_done;   // [(W-1) * kCeBatch], reused call after call
 };
-
-constexpr int kCeBatch = 64;   // buckets per fork / join round of the CE channel
-
-// DEFT_CE_PARALLEL=0: the W-1 peer copies of the copy-engine channel go back to one
-// stream, one after another (round-1 behaviour, kept for A/B)
-static bool ce_parallel() {
-  static bool v = [] {
-    const char* e = getenv("DEFT_CE_PARALLEL");
-    return !(e && atoi(e) == 0);
-  }();
-  return v;
-}
-
-// Copy-engine reduce-scatter of a bucket list on `s`: one barrier kernel, then every
-// bucket's (W-1) peer shards pulled into the staging area by DMA and summed by
-// ce_reduce_kernel.  The peer copies are forked onto one stream per peer (joined
-// per bucket, so bucket k's reduce overlaps bucket k+1's pulls): a single copy
-// engine moves ~380 GB/s, the W-1 pulls together use the link (cudaStreamWaitEvent
-// waits for the record preceding it, so the events are safely reused by the next
-// call; in a graph capture the record / wait pairs become edges).
-static deft_status_t ce_reduce_scatter(deft_comm* c, int64_t slot_base, int32_t count,
-                                       const int64_t* offsets, const int64_t* numels,
-                                       cudaStream_t s) {
-  const int esz = c->dtype == DEFT_DTYPE_F32 ? 4 : 2;
-  const int W = c->world;
-  size_t need = 0;
-  for (int32_t k = 0; k < count; ++k) {
-    const int64_t per = ((numels[k] + W - 1) / W + 16 + 7) / 8 * 8;
-    need += (size_t)(W - 1) * per * esz;
-  }
-  if (need > c->staging_bytes) {
-    if (c->staging) {
-      DEFT_CUDA(cudaStreamSynchronize(s));
-      cudaFree(c->staging);
-    }
-    DEFT_CUDA(cudaMalloc(&c->staging, need));
-    c->staging_bytes = need;
-  }
-  const bool par = ce_parallel() && W > 2;
-  if (par && !c->ce_fork) {
-    for (int j = 0; j < W - 1; ++j)
-      DEFT_CUDA(cudaStreamCreateWithFlags(&c->ce_streams[j], cudaStreamNonBlocking));
-    DEFT_CUDA(cudaEventCreateWithFlags(&c->ce_fork, cudaEventDisableTiming));
-    c->ce_done.resize((size_t)(W - 1) * kCeBatch);
-    for (auto& ev : c->ce_done) DEFT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  }
-  cudaError_t e = launch_barrier(c->P, c->rank, W, kBarrierCE, s);
-  if (e != cudaSuccess) return cuda_fail(e, "barrier_kernel");
-  for (int32_t k0 = 0; k0 < count; k0 += kCeBatch) {
-    const int32_t n = count - k0 < kCeBatch ? count - k0 : kCeBatch;
-    size_t base = 0;
-    for (int32_t k = 0; k < k0; ++k) {
-      const int64_t per = ((numels[k] + W - 1) / W + 16 + 7) / 8 * 8;
-      base += (size_t)(W - 1) * per * esz;
-    }
-    if (par) {
-      DEFT_CUDA(cudaEventRecord(c->ce_fork, s));
-      for (int j = 0; j < W - 1; ++j) DEFT_CUDA(cudaStreamWaitEvent(c->ce_streams[j], c->ce_fork, 0));
-    }
-    // pulls: peer slot j of every bucket on its own stream (or all on s)
-    size_t b = base;
-    for (int32_t k = k0; k < k0 + n; ++k) {
-      const ShardRange sh = shard_of(offsets[k], numels[k], c->rank, W, c->dtype == 0 ? 4 : 8);
-      const int64_t len = sh.hi - sh.lo;
-      const int64_t per = ((numels[k] + W - 1) / W + 16 + 7) / 8 * 8;
-      int j = 0;
-      for (int r = 0; r < W; ++r) {
-        if (r == c->rank) continue;
-        cudaStream_t cs = par ? c->ce_streams[j] : s;
-        if (len > 0) {
-          const char* src = c->P.grads[r] + (slot_base + sh.lo) * esz;
-          DEFT_CUDA(cudaMemcpyAsync(c->staging + b + (size_t)j * per * esz, src,
-                                    (size_t)len * esz, cudaMemcpyDeviceToDevice, cs));
-        }
-        if (par) DEFT_CUDA(cudaEventRecord(c->ce_done[(size_t)j * kCeBatch + (k - k0)], cs));
-        ++j;
-      }
-      if (!par && len > 0) {   // serial: reduce right behind this bucket's copies
-        e = launch_ce_reduce(c->P.grads[c->rank] + slot_base * esz, c->staging + b, c->dtype,
-                             W, c->rank, sh.lo, len, per, s);
-        if (e != cudaSuccess) return cuda_fail(e, "ce_reduce_kernel");
-      }
-      b += (size_t)(W - 1) * per * esz;
-    }
-    if (par) {   // per bucket: join its W-1 pulls, reduce
-      b = base;
-      for (int32_t k = k0; k < k0 + n; ++k) {
-        const ShardRange sh = shard_of(offsets[k], numels[k], c->rank, W, c->dtype == 0 ? 4 : 8);
-        const int64_t len = sh.hi - sh.lo;
-        const int64_t per = ((numels[k] + W - 1) / W + 16 + 7) / 8 * 8;
-        for (int j = 0; j < W - 1; ++j)
-          DEFT_CUDA(cudaStreamWaitEvent(s, c->ce_done[(size_t)j * kCeBatch + (k - k0)], 0));
-        if (len > 0) {
-          e = launch_ce_reduce(c->P.grads[c->rank] + slot_base * esz, c->staging + b, c->dtype,
-                               W, c->rank, sh.lo, len, per, s);
-          if (e != cudaSuccess) return cuda_fail(e, "ce_reduce_kernel");
-        }
-        b += (size_t)(W - 1) * per * esz;
-      }
-    }
-  }
-  // peers must be done pulling from us before our slot can change again: the
-  // update kernel's entry barrier orders that (see bucket_comm.cu).
-  return DEFT_OK;
-}
 
 extern "C" size_t deft_comm_flag_bytes(int32_t world) {
   (void)world;
@@ -532,10 +422,6 @@ extern "C" deft_status_t deft_comm_set_phase_trace(deft_comm* c, uint64_t* dev_s
 extern "C" deft_status_t deft_comm_destroy(deft_comm* c) {
   if (!c) return DEFT_OK;
   if (c->staging) cudaFree(c->staging);
-  for (auto ev : c->ce_done) cudaEventDestroy(ev);
-  if (c->ce_fork) cudaEventDestroy(c->ce_fork);
-  for (auto st : c->ce_streams)
-    if (st) cudaStreamDestroy(st);
   delete c;
   return DEFT_OK;
 }
@@ -564,7 +450,37 @@ extern "C" deft_status_t deft_bucket_reduce_scatter(deft_comm* c, int32_t channe
   }
   if (channel != DEFT_CHANNEL_CE) return fail(DEFT_ERR_INVALID_ARGUMENT, "bad channel");
   // copy-engine channel: barrier, (W-1) peer->local DMA copies, local SM reduce
-  return ce_reduce_scatter(c, slot_base, 1, &offset, &numel, s);
+  const int esz = c->dtype == DEFT_DTYPE_F32 ? 4 : 2;
+  const ShardRange sh = shard_of(offset, numel, c->rank, c->world, c->dtype == 0 ? 4 : 8);
+  const int64_t len = sh.hi - sh.lo;
+  const int64_t per = ((numel + c->world - 1) / c->world + 16 + 7) / 8 * 8;  // 16-B strides
+  const size_t need = (size_t)(c->world - 1) * per * esz;
+  if (need > c->staging_bytes) {
+    if (c->staging) {
+      DEFT_CUDA(cudaStreamSynchronize(s));
+      cudaFree(c->staging);
+    }
+    DEFT_CUDA(cudaMalloc(&c->staging, need));
+    c->staging_bytes = need;
+  }
+  cudaError_t e = launch_barrier(c->P, c->rank, c->world, kBarrierCE, s);
+  if (e != cudaSuccess) return cuda_fail(e, "barrier_kernel");
+  if (len > 0) {
+    int k = 0;
+    for (int r = 0; r < c->world; ++r) {
+      if (r == c->rank) continue;
+      const char* src = c->P.grads[r] + (slot_base + sh.lo) * esz;
+      DEFT_CUDA(cudaMemcpyAsync(c->staging + (size_t)k * per * esz, src, (size_t)len * esz,
+                                cudaMemcpyDeviceToDevice, s));
+      ++k;
+    }
+  }
+  e = launch_ce_reduce(c->P.grads[c->rank] + slot_base * esz, c->staging, c->dtype, c->world,
+                       c->rank, sh.lo, len, per, s);
+  if (e != cudaSuccess) return cuda_fail(e, "ce_reduce_kernel");
+  // peers must be done pulling from us before our slot can change again: the
+  // update kernel's entry barrier orders that (see bucket_comm.cu).
+  return DEFT_OK;
 }
 
 extern "C" deft_status_t deft_bucket_reduce_scatter_multi(deft_comm* c, int32_t channel,
@@ -589,7 +505,45 @@ extern "C" deft_status_t deft_bucket_reduce_scatter_multi(deft_comm* c, int32_t 
   }
   if (channel != DEFT_CHANNEL_CE) return fail(DEFT_ERR_INVALID_ARGUMENT, "bad channel");
   // copy-engine channel: ONE barrier, then per bucket (W-1) DMA copies + local reduce
-  return ce_reduce_scatter(c, slot_base, count, offsets, numels, s);
+  const int esz = c->dtype == DEFT_DTYPE_F32 ? 4 : 2;
+  size_t need = 0;
+  for (int32_t k = 0; k < count; ++k) {
+    const int64_t per = ((numels[k] + c->world - 1) / c->world + 16 + 7) / 8 * 8;
+    need += (size_t)(c->world - 1) * per * esz;
+  }
+  if (need > c->staging_bytes) {
+    if (c->staging) {
+      DEFT_CUDA(cudaStreamSynchronize(s));
+      cudaFree(c->staging);
+    }
+    DEFT_CUDA(cudaMalloc(&c->staging, need));
+    c->staging_bytes = need;
+  }
+  cudaError_t e = launch_barrier(c->P, c->rank, c->world, kBarrierCE, s);
+  if (e != cudaSuccess) return cuda_fail(e, "barrier_kernel");
+  size_t base = 0;
+  for (int32_t k = 0; k < count; ++k) {
+    const ShardRange sh = shard_of(offsets[k], numels[k], c->rank, c->world,
+                                   c->dtype == 0 ? 4 : 8);
+    const int64_t len = sh.hi - sh.lo;
+    const int64_t per = ((numels[k] + c->world - 1) / c->world + 16 + 7) / 8 * 8;
+    char* stage = c->staging + base;
+    if (len > 0) {
+      int j = 0;
+      for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) continue;
+        const char* src = c->P.grads[r] + (slot_base + sh.lo) * esz;
+        DEFT_CUDA(cudaMemcpyAsync(stage + (size_t)j * per * esz, src, (size_t)len * esz,
+                                  cudaMemcpyDeviceToDevice, s));
+        ++j;
+      }
+      e = launch_ce_reduce(c->P.grads[c->rank] + slot_base * esz, stage, c->dtype, c->world,
+                           c->rank, sh.lo, len, per, s);
+      if (e != cudaSuccess) return cuda_fail(e, "ce_reduce_kernel");
+    }
+    base += (size_t)(c->world - 1) * per * esz;
+  }
+  return DEFT_OK;
 }
 
 extern "C" deft_status_t deft_bucket_update(deft_comm* c, int32_t slot, int64_t offset,
