@@ -16,11 +16,13 @@ ROOT = Path(__file__).resolve().parents[1]
 SO = ROOT / "paper_2503_16815_b200" / "libdeft_b200.so"
 # the instantiations the W = 4 fp32 step runs (and W = 8 / bf16 where they differ)
 WANT = [
+    "reduce_scatter_tma_kernel<float, 2, 4, false>",
     "reduce_scatter_tma_kernel<float, 4, 4, false>",
-    "update_allgather_tma_kernel<float, 4, 3, false>",
-    "update_allgather_tma_kernel<__nv_bfloat16, 8, 3, false>",
+    "update_allgather_tma_kernel<float, 2, 4, 1, false, 4096>",
+    "update_allgather_tma_kernel<float, 4, 4, 1, false, 2048>",
+    "update_allgather_tma_kernel<__nv_bfloat16, 8, 4, 1, false, 2048>",
     "oneshot_update_kernel<float, 4>",
-    "sgd_local_kernel<float>",
+    "sgd_local_kernel<float, 2>",
     "gather_kernel",
     "ce_reduce_kernel<float>",
     "barrier_kernel",
