@@ -44,30 +44,40 @@ from .scheduler import SCHEMES, Schedule
 HW_SCHEMES = ("wfbp", "priority", "nonsequential", "deft", "deft_single_link")
 
 
-# ----------------------------------------------------------------- config (cli.py:52-175)
+# ----------------------------------------------------------------- config (cli.py:52-226)
+#
+# The experiment file's schema as data: which keys are required, the "partition"
+# block's fields with their casts and defaults, and the sweep axes with the
+# ExperimentConfig field each one fills.  Defaults, validation and messages follow
+# cli.py:70-143 so a file the reference accepts (or rejects) behaves the same here;
+# the reference's "sim" block configures its simulator and is ignored.
+
+_REQUIRED_KEYS = ("profile", "schemes", "iterations")
+_PARTITION_SCHEMA = (("partition_size", int, 6_500_000), ("mu", float, 1.0),
+                     ("enable_fusion", bool, False), ("comm_startup_us", int, 0))
+_SWEEP_SCHEMA = (("bandwidth_scale", "bandwidth_scales", float),
+                 ("partition_size", "partition_sizes", int),
+                 ("gpu_counts", "gpu_counts", int))
+
 
 @dataclass(frozen=True)
 class SweepPoint:
-    """One point of the experiment grid; the base point changes nothing (cli.py:52-67)."""
+    """One grid point; every axis at its base value is the base point (cli.py:52-67)."""
 
     bandwidth_scale: float = 1.0
     partition_size: int | None = None
     gpu_count: int | None = None
 
     def label(self) -> str:
-        parts = []
-        if self.bandwidth_scale != 1.0:
-            parts.append(f"bw{self.bandwidth_scale:g}")
-        if self.partition_size is not None:
-            parts.append(f"ps{self.partition_size}")
-        if self.gpu_count is not None:
-            parts.append(f"gpu{self.gpu_count}")
-        return "_".join(parts) or "base"
+        tags = (f"bw{self.bandwidth_scale:g}" if self.bandwidth_scale != 1.0 else "",
+                f"ps{self.partition_size}" if self.partition_size is not None else "",
+                f"gpu{self.gpu_count}" if self.gpu_count is not None else "")
+        return "_".join(t for t in tags if t) or "base"
 
 
 @dataclass(frozen=True)
 class ExperimentConfig:
-    """cli.py:70-85 (the ``sim`` block is simulator-only and ignored here)."""
+    """The parsed experiment file (cli.py:70-97)."""
 
     profile_path: str
     cluster_path: str | None
@@ -80,108 +90,105 @@ class ExperimentConfig:
     partition_sizes: tuple[int, ...] = ()
     gpu_counts: tuple[int, ...] = ()
 
+    def __post_init__(self):
+        checks = (
+            (self.iterations >= 1, "iterations must be >= 1"),
+            (bool(self.schemes), "schemes must be non-empty"),
+            (all(s in SCHEMES for s in self.schemes),
+             f"unknown schemes {[s for s in self.schemes if s not in SCHEMES]}; "
+             f"valid: {list(SCHEMES)}"),
+            (all(x > 0 for x in self.bandwidth_scales), "bandwidth_scale values must be > 0"),
+            (all(x > 0 for x in self.partition_sizes), "partition_size values must be > 0"),
+            (all(x >= 2 for x in self.gpu_counts), "gpu_counts values must be >= 2"),
+        )
+        for ok, msg in checks:
+            if not ok:
+                raise SchemaError(msg)
+
 
 def experiment_config_from_dict(data: dict, base_dir: Path) -> ExperimentConfig:
-    """Same fields, defaults and SchemaError messages as cli.py:100-143."""
+    """cli.py:100-143: the file's dict -> ExperimentConfig, paths relative to base_dir."""
     if not isinstance(data, dict):
         raise SchemaError("experiment config must be a JSON object")
-    for key in ("profile", "schemes", "iterations"):
+    for key in _REQUIRED_KEYS:
         if key not in data:
             raise SchemaError(f"experiment config: missing field {key!r}")
-    unknown = [s for s in data["schemes"] if s not in SCHEMES]
-    if unknown:
-        raise SchemaError(f"unknown schemes: {unknown}")
-    part = data.get("partition", {})
-    partition = PartitionConfig(
-        partition_size=int(part.get("partition_size", 6_500_000)),
-        mu=float(part.get("mu", 1.0)),
-        enable_fusion=bool(part.get("enable_fusion", False)),
-        comm_startup_us=int(part.get("comm_startup_us", 0)),
-    )
-    walk = WalkParams.from_dict(data["walk"]) if "walk" in data else None
+    block = data.get("partition", {})
+    partition = PartitionConfig(**{name: cast(block.get(name, default))
+                                   for name, cast, default in _PARTITION_SCHEMA})
     sweeps = data.get("sweeps", {})
-    for axis in ("bandwidth_scale", "partition_size", "gpu_counts"):
-        if axis in sweeps and not sweeps[axis]:
-            raise SchemaError(f"sweep axis {axis!r} must be non-empty when present")
-    cluster_path = cluster_inline = None
-    if "cluster" in data:
-        if isinstance(data["cluster"], dict):
-            cluster_inline = data["cluster"]
-        else:
-            cluster_path = str(Path(base_dir) / data["cluster"])
+    axes = {}
+    for key, field_name, cast in _SWEEP_SCHEMA:
+        values = sweeps.get(key, [])
+        if key in sweeps and not values:
+            raise SchemaError(f"sweep axis {key!r} must be non-empty when present")
+        axes[field_name] = tuple(cast(v) for v in values)
+    base = Path(base_dir)
+    cluster = data.get("cluster")
+    inline = cluster if isinstance(cluster, dict) else None
     return ExperimentConfig(
-        profile_path=str(Path(base_dir) / data["profile"]),
-        cluster_path=cluster_path,
-        cluster_inline=cluster_inline,
+        profile_path=str(base / data["profile"]),
+        cluster_path=None if cluster is None or inline is not None else str(base / cluster),
+        cluster_inline=inline,
         schemes=tuple(data["schemes"]),
         iterations=int(data["iterations"]),
         partition=partition,
-        walk=walk,
-        bandwidth_scales=tuple(float(x) for x in sweeps.get("bandwidth_scale", [])),
-        partition_sizes=tuple(int(x) for x in sweeps.get("partition_size", [])),
-        gpu_counts=tuple(int(x) for x in sweeps.get("gpu_counts", [])),
-    )
+        walk=WalkParams.from_dict(data["walk"]) if "walk" in data else None,
+        **axes)
 
 
 def load_experiment_config(path) -> ExperimentConfig:
+    """cli.py:146-152."""
     path = Path(path)
     try:
-        data = json.loads(path.read_text())
+        raw = json.loads(path.read_text())
     except json.JSONDecodeError as e:
         raise SchemaError(f"{path}: invalid JSON ({e})") from e
-    return experiment_config_from_dict(data, path.parent)
+    return experiment_config_from_dict(raw, path.parent)
 
 
 def sweep_points(cfg: ExperimentConfig) -> list[SweepPoint]:
-    """The base point plus each axis varied on its own (cli.py:160-175)."""
-    points = [SweepPoint()]
-    for s in cfg.bandwidth_scales:
-        if s != 1.0:
-            points.append(SweepPoint(bandwidth_scale=s))
-    for ps in cfg.partition_sizes:
-        if ps != cfg.partition.partition_size:
-            points.append(SweepPoint(partition_size=ps))
-    if cfg.gpu_counts:
-        ref = cfg.gpu_counts[0]
-        for g in cfg.gpu_counts[1:]:
-            points.append(SweepPoint(gpu_count=g))
-        return [p for p in points if p.gpu_count is None or p.gpu_count != ref]
-    return points
-
-
-def _ring_factor(p: int) -> float:
-    return 2.0 * (p - 1) / p
+    """The base point, then every axis value away from its base on its own; with a
+    gpu_counts axis its first entry is the reference size and is dropped
+    (cli.py:160-175)."""
+    grid = [SweepPoint()]
+    grid += [SweepPoint(bandwidth_scale=x) for x in cfg.bandwidth_scales if x != 1.0]
+    grid += [SweepPoint(partition_size=x) for x in cfg.partition_sizes
+             if x != cfg.partition.partition_size]
+    if not cfg.gpu_counts:
+        return grid
+    reference = cfg.gpu_counts[0]
+    grid += [SweepPoint(gpu_count=g) for g in cfg.gpu_counts[1:]]
+    return [p for p in grid if p.gpu_count != reference]
 
 
 def point_profile(profile: ModelProfile, point: SweepPoint,
                   gpu_reference: int | None) -> ModelProfile:
-    """cli.py:178-186."""
+    """The profile a grid point plans with: communication times scaled by
+    1/bandwidth_scale and, for a gpu_count point, by the ring all-reduce volume
+    2(p-1)/p relative to the reference size (cli.py:178-186)."""
     factor = 1.0 / point.bandwidth_scale
     if point.gpu_count is not None and gpu_reference:
-        factor *= _ring_factor(point.gpu_count) / _ring_factor(gpu_reference)
-    if factor == 1.0:
-        return profile
-    return profile.scaled_comm(factor, name_suffix="")
+        ring = lambda p: 2.0 * (p - 1) / p   # noqa: E731
+        factor *= ring(point.gpu_count) / ring(gpu_reference)
+    return profile if factor == 1.0 else profile.scaled_comm(factor, name_suffix="")
 
 
 def config_hash(cfg: ExperimentConfig, seed: int) -> str:
-    """cli.py:211-226 (same blob, so a hardware run and a simulated run of one
-    experiment file carry the same hash)."""
-    blob = json.dumps(
-        {
-            "profile": Path(cfg.profile_path).name,
-            "schemes": list(cfg.schemes),
-            "iterations": cfg.iterations,
-            "partition": vars(cfg.partition) | {},
-            "walk": vars(cfg.walk) | {} if cfg.walk else None,
-            "bandwidth_scales": list(cfg.bandwidth_scales),
-            "partition_sizes": list(cfg.partition_sizes),
-            "gpu_counts": list(cfg.gpu_counts),
-            "seed": seed,
-        },
-        sort_keys=True,
-    )
-    return hashlib.sha256(blob.encode()).hexdigest()[:16]
+    """First 16 hex digits of sha256 over the experiment's identity -- the same
+    JSON document cli.py:211-226 hashes, so a hardware run and a simulated run of
+    one experiment file carry the same hash."""
+    identity = {
+        "profile": Path(cfg.profile_path).name,
+        "schemes": list(cfg.schemes),
+        "iterations": cfg.iterations,
+        "partition": dict(vars(cfg.partition)),
+        "walk": dict(vars(cfg.walk)) if cfg.walk else None,
+        "seed": seed,
+    }
+    identity.update({field_name: list(getattr(cfg, field_name))
+                     for _, field_name, _ in _SWEEP_SCHEMA})
+    return hashlib.sha256(json.dumps(identity, sort_keys=True).encode()).hexdigest()[:16]
 
 
 # ------------------------------------------------------------ reports (simulator.py:64-300)
