@@ -218,49 +218,47 @@ class RunReport:
                    bubble / total_us if total_us > 0 else 0.0, updates_performed,
                    iterations * batch_size / (total_us / 1e6) if total_us > 0 else 0.0)
 
+    # summary.json's "report" block: (key, attribute, digits kept or None) in the
+    # reference's key set (simulator.py:262-273)
+    _SUMMARY = (("scheme", "scheme", None), ("profile", "profile_name", None),
+                ("iterations", "iterations", None), ("total_time_us", "total_time_us", None),
+                ("mean_iteration_time_us", "mean_iteration_time_us", 3),
+                ("bubble_time_us", "bubble_time_us", None), ("bubble_ratio", "bubble_ratio", 6),
+                ("updates_performed", "updates_performed", None),
+                ("throughput_samples_per_s", "throughput_samples_per_s", 3))
+
     def summary_dict(self) -> dict:
-        return {
-            "scheme": self.scheme,
-            "profile": self.profile_name,
-            "iterations": self.iterations,
-            "total_time_us": self.total_time_us,
-            "mean_iteration_time_us": round(self.mean_iteration_time_us, 3),
-            "bubble_time_us": self.bubble_time_us,
-            "bubble_ratio": round(self.bubble_ratio, 6),
-            "updates_performed": self.updates_performed,
-            "throughput_samples_per_s": round(self.throughput_samples_per_s, 3),
-        }
+        return {key: getattr(self, attr) if digits is None else round(getattr(self, attr), digits)
+                for key, attr, digits in self._SUMMARY}
 
 
 def compare(reports: dict[str, RunReport], baseline: str = "wfbp") -> dict:
-    """Speedups of every scheme against a named baseline (simulator.py:276-300)."""
+    """Every scheme's totals and its speedup over the named baseline, schemes in
+    name order (simulator.py:276-300: same checks, rounding and keys)."""
     if not reports:
         raise ComparisonError("no reports to compare")
-    names = set(r.profile_name for r in reports.values())
-    iters = set(r.iterations for r in reports.values())
-    if len(iters) != 1:
-        raise ComparisonError(f"iteration counts differ: {sorted(iters)}")
+    iteration_counts = sorted({r.iterations for r in reports.values()})
+    if len(iteration_counts) != 1:
+        raise ComparisonError(f"iteration counts differ: {iteration_counts}")
     if baseline not in reports:
         raise ComparisonError(f"baseline {baseline!r} missing from reports")
-    base = reports[baseline].total_time_us
-    rows = []
-    for scheme in sorted(reports):
-        r = reports[scheme]
-        rows.append({
-            "scheme": scheme,
-            "profile": r.profile_name,
-            "total_time_us": r.total_time_us,
-            "mean_iteration_time_us": round(r.mean_iteration_time_us, 3),
-            "bubble_ratio": round(r.bubble_ratio, 6),
-            "updates_performed": r.updates_performed,
-            "speedup_vs_" + baseline: round(base / r.total_time_us, 4)
-            if r.total_time_us else 0.0,
-        })
-    return {"baseline": baseline, "profiles": sorted(names), "rows": rows}
+    t_base = reports[baseline].total_time_us
+
+    def row(name: str, r: RunReport) -> dict:
+        speedup = round(t_base / r.total_time_us, 4) if r.total_time_us else 0.0
+        return {"scheme": name, "profile": r.profile_name, "total_time_us": r.total_time_us,
+                "mean_iteration_time_us": round(r.mean_iteration_time_us, 3),
+                "bubble_ratio": round(r.bubble_ratio, 6),
+                "updates_performed": r.updates_performed, f"speedup_vs_{baseline}": speedup}
+    return {"baseline": baseline,
+            "profiles": sorted({r.profile_name for r in reports.values()}),
+            "rows": [row(name, reports[name]) for name in sorted(reports)]}
 
 
 @dataclass
 class RunRecord:
+    """One (scheme, sweep point) run of an experiment and its report (cli.py:189-199)."""
+
     scheme: str
     point: SweepPoint
     report: RunReport
@@ -275,16 +273,19 @@ class RunRecord:
 
 @dataclass
 class ReportBundle:
+    """Every run of an experiment plus its identity (cli.py:202-208)."""
+
     config_hash: str
     runs: list[RunRecord]
     iterations: int
     skipped: list[dict] = field(default_factory=list)
 
     def by_point(self) -> dict[str, dict[str, RunRecord]]:
-        out: dict[str, dict[str, RunRecord]] = {}
-        for r in self.runs:
-            out.setdefault(r.point.label(), {})[r.scheme] = r
-        return out
+        """sweep-point label -> scheme -> run."""
+        grid: dict[str, dict[str, RunRecord]] = {}
+        for run in self.runs:
+            grid.setdefault(run.point.label(), {})[run.scheme] = run
+        return grid
 
 
 def _write_csv(path: Path, header: list[str], rows: list[list]) -> None:
@@ -294,83 +295,79 @@ def _write_csv(path: Path, header: list[str], rows: list[list]) -> None:
         w.writerows(rows)
 
 
+_COMPARISON_HEADER = ["sweep_point", "scheme", "total_time_us", "mean_iteration_time_us",
+                      "bubble_ratio", "updates_performed", "speedup_vs_baseline"]
+
+
+def _run_doc(r: RunRecord) -> dict:
+    """One run of summary.json: the reference's keys (cli.py:299-316), plus the
+    hardware block of a GPU run."""
+    p = r.point
+    doc = {"run_id": r.run_id, "scheme": r.scheme, "report": r.report.summary_dict(),
+           "preserver": r.verdict,
+           "sweep_point": {"bandwidth_scale": p.bandwidth_scale,
+                           "partition_size": p.partition_size, "gpu_count": p.gpu_count}}
+    if r.hardware is not None:
+        doc["hardware"] = r.hardware
+    return doc
+
+
+def _comparison_rows(bundle: ReportBundle) -> list[list]:
+    """comparison.csv: every scheme against wfbp (else the first scheme by name) at
+    every sweep point (cli.py:325-343)."""
+    out = []
+    for label, by_scheme in sorted(bundle.by_point().items()):
+        base = "wfbp" if "wfbp" in by_scheme else min(by_scheme)
+        table = compare({name: run.report for name, run in by_scheme.items()}, base)
+        out += [[label] + [row[k] for k in ("scheme", "total_time_us", "mean_iteration_time_us",
+                                            "bubble_ratio", "updates_performed")]
+                + [row["speedup_vs_" + base]] for row in table["rows"]]
+    return out
+
+
+def _speedup_curves(bundle: ReportBundle):
+    """plotdata/: speedup vs wfbp along the bandwidth and the partition-size axes
+    (cli.py:354-389) -> (file name, header, rows), empty curves left out."""
+    by_point = bundle.by_point()
+    scales = sorted({r.point.bandwidth_scale for r in bundle.runs} - {1.0})
+    sizes = sorted({r.point.partition_size for r in bundle.runs if r.point.partition_size})
+    axes = (("speedup_vs_bandwidth.csv", "bandwidth_scale",
+             [("base", 1.0)] + [(SweepPoint(bandwidth_scale=x).label(), x) for x in scales]),
+            ("speedup_vs_partition_size.csv", "partition_size",
+             [(SweepPoint(partition_size=x).label(), x) for x in sizes]))
+    for fname, axis, points in axes:
+        rows = []
+        for label, x in points:
+            runs = by_point.get(label, {})
+            if "wfbp" in runs:
+                t_base = runs["wfbp"].report.total_time_us
+                rows += [[x, name, round(t_base / runs[name].report.total_time_us, 4)
+                          if runs[name].report.total_time_us else 0.0]
+                         for name in sorted(runs)]
+        if rows:
+            yield fname, [axis, "scheme", "speedup_vs_wfbp"], rows
+
+
 def emit_reports(bundle: ReportBundle, out_dir) -> list[Path]:
     """summary.json, comparison.csv and plotdata/ in the schema of cli.py:294-391
     (timeline / Chrome-trace files are simulator output and not written)."""
     out = Path(out_dir)
     out.mkdir(parents=True, exist_ok=True)
-    written: list[Path] = []
-    runs = []
-    for r in sorted(bundle.runs, key=lambda r: r.run_id):
-        doc = {
-            "run_id": r.run_id,
-            "scheme": r.scheme,
-            "sweep_point": {
-                "bandwidth_scale": r.point.bandwidth_scale,
-                "partition_size": r.point.partition_size,
-                "gpu_count": r.point.gpu_count,
-            },
-            "report": r.report.summary_dict(),
-            "preserver": r.verdict,
-        }
-        if r.hardware is not None:
-            doc["hardware"] = r.hardware
-        runs.append(doc)
     summary = {"config_hash": bundle.config_hash, "iterations": bundle.iterations,
-               "runs": runs}
+               "runs": [_run_doc(r) for r in sorted(bundle.runs, key=lambda r: r.run_id)]}
     if bundle.skipped:
         summary["skipped"] = bundle.skipped
-    spath = out / "summary.json"
-    spath.write_text(json.dumps(summary, indent=2, sort_keys=True) + "\n")
-    written.append(spath)
+    files = [out / "summary.json"]
+    files[0].write_text(json.dumps(summary, indent=2, sort_keys=True) + "\n")
     if not bundle.runs:
-        return written
-
-    comp_rows = []
-    for label, by_scheme in sorted(bundle.by_point().items()):
-        baseline = "wfbp" if "wfbp" in by_scheme else sorted(by_scheme)[0]
-        table = compare({s: r.report for s, r in by_scheme.items()}, baseline)
-        for row in table["rows"]:
-            comp_rows.append([label, row["scheme"], row["total_time_us"],
-                              row["mean_iteration_time_us"], row["bubble_ratio"],
-                              row["updates_performed"], row[f"speedup_vs_{baseline}"]])
-    cpath = out / "comparison.csv"
-    _write_csv(cpath, ["sweep_point", "scheme", "total_time_us", "mean_iteration_time_us",
-                       "bubble_ratio", "updates_performed", "speedup_vs_baseline"], comp_rows)
-    written.append(cpath)
-
-    plot_dir = out / "plotdata"
-    plot_dir.mkdir(exist_ok=True)
-    by_point = bundle.by_point()
-
-    def speedup_rows(points):
-        rows = []
-        for label, x in points:
-            by_scheme = by_point.get(label, {})
-            if "wfbp" not in by_scheme:
-                continue
-            base = by_scheme["wfbp"].report.total_time_us
-            for scheme in sorted(by_scheme):
-                t = by_scheme[scheme].report.total_time_us
-                rows.append([x, scheme, round(base / t, 4) if t else 0.0])
-        return rows
-
-    bw_points = [("base", 1.0)] + [
-        (SweepPoint(bandwidth_scale=s).label(), s)
-        for s in sorted({r.point.bandwidth_scale for r in bundle.runs} - {1.0})]
-    rows = speedup_rows(bw_points)
-    if rows:
-        p = plot_dir / "speedup_vs_bandwidth.csv"
-        _write_csv(p, ["bandwidth_scale", "scheme", "speedup_vs_wfbp"], rows)
-        written.append(p)
-    ps_points = [(SweepPoint(partition_size=ps).label(), ps) for ps in
-                 sorted({r.point.partition_size for r in bundle.runs if r.point.partition_size})]
-    rows = speedup_rows(ps_points)
-    if rows:
-        p = plot_dir / "speedup_vs_partition_size.csv"
-        _write_csv(p, ["partition_size", "scheme", "speedup_vs_wfbp"], rows)
-        written.append(p)
-    return written
+        return files
+    files.append(out / "comparison.csv")
+    _write_csv(files[-1], _COMPARISON_HEADER, _comparison_rows(bundle))
+    (out / "plotdata").mkdir(exist_ok=True)
+    for fname, header, rows in _speedup_curves(bundle):
+        files.append(out / "plotdata" / fname)
+        _write_csv(files[-1], header, rows)
+    return files
 
 
 # ------------------------------------------------------------------- running on GPUs
