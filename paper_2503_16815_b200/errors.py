@@ -95,3 +95,11 @@ def raise_for_status(status: int, what: str, detail: str = "") -> None:
     if detail:
         msg += f": {detail}"
     raise cls(msg)
+
+
+def check_rules(rules, error: type = ValueError) -> None:
+    """Validate in order: every rule is (ok, message) or (ok, message, exception
+    class); the first failing rule raises (``error`` unless the rule names one)."""
+    for rule in rules:
+        if not rule[0]:
+            raise (rule[2] if len(rule) > 2 else error)(rule[1])

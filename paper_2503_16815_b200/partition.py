@@ -9,7 +9,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 
-from .errors import InfeasiblePartitionError
+from .errors import InfeasiblePartitionError, check_rules
 from .profiles import BucketProfile, ModelProfile
 
 DEFAULT_PARTITION_SIZE = 6_500_000
@@ -25,12 +25,10 @@ class PartitionConfig:
     comm_startup_us: int = 0
 
     def __post_init__(self):
-        if self.partition_size <= 0:
-            raise InfeasiblePartitionError("partition_size must be > 0")
-        if self.mu < 1.0:
-            raise InfeasiblePartitionError("mu must be >= 1")
-        if self.comm_startup_us < 0:
-            raise InfeasiblePartitionError("comm_startup_us must be >= 0")
+        check_rules(((self.partition_size > 0, "partition_size must be > 0"),
+                     (self.mu >= 1.0, "mu must be >= 1"),
+                     (self.comm_startup_us >= 0, "comm_startup_us must be >= 0")),
+                    InfeasiblePartitionError)
 
 
 def split_evenly(total: int, parts: int) -> list[int]:
