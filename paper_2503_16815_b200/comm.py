@@ -123,7 +123,9 @@ class BucketComm:
     def set_phase_trace(self, stamps) -> None:
         """Diagnostics: a device uint64 tensor (>= 256 x 8) that the TMA reduce-
         scatter / update and one-shot kernels stamp with globaltimer ns at their
-        phase boundaries (deft_comm_set_phase_trace), or None to stop."""
+        phase boundaries (deft_comm_set_phase_trace), or None to stop.  Every launch
+        captures the pointer by value: keep the tensor alive until those launches
+        have completed (e.g. a synchronize before it is freed)."""
         ptr = None if stamps is None else _native.c_vp(stamps.data_ptr())
         check(_native.lib().deft_comm_set_phase_trace(self._h, ptr), "deft_comm_set_phase_trace")
 
