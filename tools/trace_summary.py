@@ -32,9 +32,14 @@ def main():
     streams = defaultdict(list)
     for e in evs:
         streams[e["args"].get("stream", e.get("tid"))].append(e)
-    # compute stream = the stream with the most kernel time
+    # compute stream = the stream with the most MODEL (non-DeFT, non-copy) kernel
+    # time -- under graph replay CUPTI spreads a graph's branches over several
+    # streams, and a busy link stream (copy-engine pulls, spinning barrier
+    # kernels) can out-total the compute stream
     busy = {s: sum(e["dur"] for e in v) for s, v in streams.items()}
-    comp = max(busy, key=busy.get)
+    model = {s: sum(e["dur"] for e in v if not short(e["name"]) and e["cat"] == "kernel")
+             for s, v in streams.items()}
+    comp = max(model, key=model.get)
     t0, t1 = evs[0]["ts"], max(e["ts"] + e["dur"] for e in evs)
     print(f"span {t1 - t0:.0f} us over the traced steps; streams:")
     for s, v in sorted(streams.items(), key=lambda kv: -busy[kv[0]]):
@@ -54,6 +59,21 @@ def main():
         if g > 5:
             gaps.append((g, a["ts"] - t0, a["name"][:60], b["name"][:60]))
     gaps.sort(reverse=True)
+    # union of all model-kernel activity (any stream): idle = no model kernel runs
+    iv = sorted((e["ts"], e["ts"] + e["dur"]) for e in evs
+                if e["cat"] == "kernel" and not short(e["name"]))
+    union, cur = 0.0, None
+    for a, b in iv:
+        if cur is None or a > cur[1]:
+            if cur:
+                union += cur[1] - cur[0]
+            cur = [a, b]
+        else:
+            cur[1] = max(cur[1], b)
+    if cur:
+        union += cur[1] - cur[0]
+    print(f"model kernels active {union:.0f} us of {t1 - t0:.0f} us "
+          f"({100 * union / (t1 - t0):.1f} %)")
     print(f"compute-stream idle total {sum(g for g, *_ in gaps):.0f} us in {len(gaps)} gaps > 5 us;"
           " largest:")
     for g, at, a, b in gaps[:15]:
